@@ -1,0 +1,156 @@
+/*
+ * tacsl_b200.h -- C ABI of the B200-native TacSL sensor-simulation hot path.
+ *
+ * One shared library (libtacsl_b200.so, sm_100a) exporting plain C entry
+ * points: no torch types, plain device pointers + sizes, stream-ordered,
+ * re-entrant.  Every call returns TACSL_OK (0) or an error code; the message
+ * of the last failing call on the calling thread is tacsl_last_error().
+ *
+ * Each entry point replaces one function of the reference Python package
+ * `gelsim` (paths relative to /root/reference/pkg/src/gelsim):
+ *
+ *   tacsl_depth_to_rgb      render/lut.py:68-76   depth_to_rgb (+ depth_gradients
+ *                           lut.py:25-28, PolyLut.evaluate / _design_matrix
+ *                           lut.py:56-65, and to_uint8 render/imageio.py:8-11
+ *                           fused as the uint8 epilogue)
+ *   tacsl_lut_create        render/lut.py:31-54   PolyLut (coefficients + image_size)
+ *   tacsl_to_uint8          render/imageio.py:8-11 to_uint8 (standalone)
+ *   tacsl_sdf_create        geometry/sdf.py:29-54 SdfGrid (device upload)
+ *   tacsl_query_sdf         geometry/sdf.py:271-321 query_sdf
+ *   tacsl_penalty_forces    tactile/field.py:61-76 penalty_forces
+ *   tacsl_force_field       tactile/field.py:79-129 compute_force_field
+ *                           (+ net_wrench tactile/field.py:132-141 fused as a
+ *                           per-sensor reduction when `wrench` is non-NULL)
+ *   tacsl_net_wrench        tactile/field.py:132-141 net_wrench (standalone)
+ *
+ * The reference has no FFI of its own (pure numpy); the Python module
+ * paper_2408_06506_b200 binds these with ctypes behind the reference's
+ * function names and signatures.
+ *
+ * Conventions
+ *  - quaternions are (w, x, y, z) (transforms.py:3);
+ *  - a rigid-body "state" is 13 float64: pos[3], quat[4], linvel[3], angvel[3];
+ *  - every array is C-contiguous; images are (N, H, W) depth and
+ *    (N, H, W, 3) RGB (HWC interleaved, as the reference returns);
+ *  - all pointers passed to compute calls are DEVICE pointers on the
+ *    handle's device; `stream` is a cudaStream_t (NULL = legacy default).
+ */
+#ifndef TACSL_B200_H
+#define TACSL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TACSL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TACSL_API __attribute__((visibility("default")))
+#else
+#define TACSL_API
+#endif
+
+typedef enum {
+  TACSL_OK = 0,
+  TACSL_ERR_INVALID_ARGUMENT = 1,       /* -> ValueError                       */
+  TACSL_ERR_DIMENSION_MISMATCH = 2,     /* -> gelsim.errors.DimensionMismatch  */
+  TACSL_ERR_LUT_RESOLUTION_MISMATCH = 3,/* -> gelsim.errors.LutResolutionMismatch */
+  TACSL_ERR_INVALID_QUERY = 4,          /* -> gelsim.errors.InvalidQuery       */
+  TACSL_ERR_CUDA = 5,                   /* -> RuntimeError (CUDA failure)      */
+  TACSL_ERR_NO_DEVICE = 6               /* -> RuntimeError (no sm_100 device)  */
+} tacsl_status_t;
+
+typedef struct tacsl_lut_s* tacsl_lut_t;
+typedef struct tacsl_sdf_s* tacsl_sdf_t;
+
+/* PenaltyParams (tactile/field.py:28-37). */
+typedef struct {
+  double k_n;  /* normal stiffness, N/m            */
+  double k_d;  /* normal damping on d*d_dot        */
+  double k_t;  /* shear stiffness vs slip speed    */
+  double mu;   /* friction coefficient             */
+} tacsl_penalty_t;
+
+TACSL_API int tacsl_abi_version(void);
+TACSL_API const char* tacsl_last_error(void);
+/* 1 if `device` is an sm_100 part the library has code for, else 0. */
+TACSL_API int tacsl_device_supported(int device);
+
+/* ---------------------------------------------------------------- LUT --- */
+/* coeffs: HOST (3, n_terms) float64 in monomial_exponents(degree) order
+ * (lut.py:20-22); degree in [2,4] (lut.py:47-48) else INVALID_ARGUMENT.
+ * width/height: the image_size the LUT was calibrated at (W, H). */
+TACSL_API int tacsl_lut_create(const double* coeffs, int degree, int width, int height,
+                     tacsl_lut_t* out);
+TACSL_API void tacsl_lut_destroy(tacsl_lut_t lut);
+
+/* depth (N, H, W) float32 -> rgb (N, H, W, 3); either output may be NULL
+ * (not both).  rgb_u8 = clip(rint(255*x)), rgb_f32 = x in [0,1].
+ * LUT_RESOLUTION_MISMATCH when (width, height) != lut image size (lut.py:70-74);
+ * INVALID_ARGUMENT when H < 2 or W < 2 (np.gradient needs 2 samples). */
+TACSL_API int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n_images,
+                       int height, int width, uint8_t* rgb_u8, float* rgb_f32,
+                       void* stream);
+
+/* x (count) float32 -> u8 = clip(rint(255*x), 0, 255) (imageio.py:8-11). */
+TACSL_API int tacsl_to_uint8(const float* x, int64_t count, uint8_t* out, void* stream);
+
+/* ---------------------------------------------------------------- SDF --- */
+/* values: HOST (nx,ny,nz) float64, gradients: HOST (nx,ny,nz,3) float64,
+ * z fastest (sdf.py:29-41).  Uploaded as a float64 {d, gx, gy, gz} cell grid
+ * (32 B/cell, L2-resident) on `device`, so grids built in float64 by the
+ * reference's build_sdf and float32 TSDF caches (sdf.py:343-344) are both
+ * sampled exactly as the reference samples them.  dims >= 2 on every axis,
+ * spacing > 0, else INVALID_ARGUMENT. */
+TACSL_API int tacsl_sdf_create(int device, const double* values, const double* gradients,
+                     const int32_t dims[3], const double origin[3],
+                     double spacing, tacsl_sdf_t* out);
+TACSL_API void tacsl_sdf_destroy(tacsl_sdf_t sdf);
+
+/* points (n, 3) float64 -> distance (n) float64 (+inf when outside),
+ * normal (n, 3) float64 (0 when outside), valid (n) uint8.  Any output may
+ * be NULL. */
+TACSL_API int tacsl_query_sdf(tacsl_sdf_t sdf, const double* points, int64_t n,
+                    double* distance, double* normal, uint8_t* valid,
+                    void* stream);
+
+/* -------------------------------------------------------- force field --- */
+/* Elementwise penalty formulas on `count` points, all float64:
+ * d (count), d_dot (count), n (count,3), v_t (count,3) -> f_n, f_t (count,3).
+ * INVALID_ARGUMENT when any parameter is negative (field.py:35-37). */
+TACSL_API int tacsl_penalty_forces(const double* d, const double* d_dot, const double* n,
+                         const double* v_t, int64_t count, tacsl_penalty_t params,
+                         double* f_n, double* f_t, void* stream);
+
+/* Force field of n_envs x n_sensors sensor frames against one object SDF.
+ *   taxels        (rows*cols, 3) float64, sensor frame (points.py:33-67)
+ *   object_state  env e at object_state + e*object_stride   (13 doubles;
+ *                 stride 0 broadcasts one state to every env)
+ *   sensor_state  (e, s) at sensor_state + e*sensor_stride + s*13
+ *   out_fp64      0: f_n/f_t are float32, 1: float64; layout (E, S, R, C, 3),
+ *                 sensor frame (field.py:118-119)
+ *   wrench        nullable (E, S, 6) float64 = force[3], torque[3] about the
+ *                 sensor origin (field.py:132-141)
+ *   kin           nullable (E, S, R, C, 8) float64 = d, d_dot, v_t[3], n[3]
+ *                 (world frame, field.py:123-129)
+ *   contact       nullable (E, S, R, C) uint8 = (d < 0) (field.py:64)
+ */
+TACSL_API int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
+                      const double* object_state, int64_t object_stride,
+                      const double* sensor_state, int64_t sensor_stride,
+                      int64_t n_envs, int n_sensors, tacsl_penalty_t params,
+                      int out_fp64, void* f_n, void* f_t, double* wrench,
+                      double* kin, uint8_t* contact, void* stream);
+
+/* net_wrench on an existing field: f_n, f_t (frames, rows, cols, 3) float64,
+ * points (rows, cols, 3) float64 -> force, torque (frames, 3) float64. */
+TACSL_API int tacsl_net_wrench(const double* f_n, const double* f_t, const double* points,
+                     int64_t frames, int rows, int cols, double* force,
+                     double* torque, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TACSL_B200_H */

@@ -1,0 +1,56 @@
+"""Device plumbing: torch owns device memory and streams; kernels come from
+libtacsl_b200.so.  No CPU fallback -- every entry point requires a B200."""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+def torch():
+    import torch as _t  # local import keeps `import paper_2408_06506_b200` light
+
+    return _t
+
+
+def resolve_device(device=None):
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError(
+            "paper_2408_06506_b200 runs on a CUDA B200 (sm_100a) device only; "
+            "torch.cuda.is_available() is False and there is no CPU fallback")
+    if device is None:
+        dev = t.device("cuda", t.cuda.current_device())
+    else:
+        dev = t.device(device)
+        if dev.type != "cuda":
+            raise RuntimeError(f"device {dev} is not a CUDA device; there is no CPU fallback")
+        if dev.index is None:
+            dev = t.device("cuda", t.cuda.current_device())
+    lib = _lib.load()
+    if not lib.tacsl_device_supported(dev.index):
+        raise RuntimeError(f"cuda:{dev.index} is not an sm_100 (B200) GPU; libtacsl_b200 has sm_100a code only")
+    return dev
+
+
+def is_cuda_tensor(x) -> bool:
+    t = torch()
+    return isinstance(x, t.Tensor) and x.is_cuda
+
+
+def to_device(x, dtype, device):
+    """numpy / python / torch -> contiguous torch tensor of `dtype` on `device`."""
+    t = torch()
+    if isinstance(x, t.Tensor):
+        return x.to(device=device, dtype=dtype).contiguous()
+    np_dtype = {t.float32: np.float32, t.float64: np.float64, t.uint8: np.uint8}[dtype]
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np_dtype))
+    return t.from_numpy(arr).to(device)
+
+
+def stream_handle(device) -> int:
+    return torch().cuda.current_stream(device).cuda_stream
+
+
+def ptr(x) -> int | None:
+    return None if x is None else x.data_ptr()

@@ -1,0 +1,32 @@
+// Opaque handle layouts shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tacsl {
+
+// Polynomial LUT coefficients, monomial order of render/lut.py:20-22,
+// pre-scaled by 2^-(i+j) (see api.cu fill_scaled).  Passed to kernels BY
+// VALUE, so the coefficients live in the constant bank and feed FFMA
+// operands directly.
+struct LutParams {
+  float c[3][15];
+};
+
+}  // namespace tacsl
+
+struct tacsl_lut_s {
+  int degree;
+  int width;
+  int height;
+  tacsl::LutParams params;
+};
+
+struct tacsl_sdf_s {
+  int device;
+  double2* grid;  // (nx, ny, nz) x {(d, gx), (gy, gz)}, z fastest
+  int dims[3];
+  double origin[3];
+  double spacing;
+};

@@ -1,0 +1,72 @@
+"""Rebind the reference's hot-path names to the B200 implementations.
+
+The reference binds names at import time (``from ..render.lut import
+depth_to_rgb`` etc.), so every importing module must be rebound, not just
+the defining one:
+
+    gelsim.render, gelsim.render.lut          depth_to_rgb
+    gelsim.render, gelsim.render.imageio      to_uint8
+    gelsim.tactile, gelsim.tactile.field      compute_force_field, penalty_forces, net_wrench
+    gelsim.envs.peg_tasks, gelsim.envs.scenes depth_to_rgb, compute_force_field
+    gelsim.geometry, gelsim.geometry.sdf      query_sdf (standalone API only)
+
+``query_sdf`` is deliberately NOT rebound at the physics call sites
+(physics/contacts.py:15, envs/peg_tasks.py _fit_grip): those are tiny CPU
+queries where a device round trip would only add latency; inside
+``compute_force_field`` the query is fused into K2 anyway.
+"""
+from __future__ import annotations
+
+import importlib
+
+_SITES = {
+    "gelsim.render": ("depth_to_rgb", "to_uint8"),
+    "gelsim.render.lut": ("depth_to_rgb",),
+    "gelsim.render.imageio": ("to_uint8",),
+    "gelsim.tactile": ("compute_force_field", "penalty_forces", "net_wrench"),
+    "gelsim.tactile.field": ("compute_force_field", "penalty_forces", "net_wrench"),
+    "gelsim.envs.peg_tasks": ("depth_to_rgb", "compute_force_field"),
+    "gelsim.envs.scenes": ("depth_to_rgb", "compute_force_field"),
+    "gelsim.geometry": ("query_sdf",),
+}
+
+_saved: dict = {}
+
+
+def _impl(name):
+    from . import geometry, render, tactile
+
+    return {
+        "depth_to_rgb": render.depth_to_rgb,
+        "to_uint8": render.to_uint8,
+        "compute_force_field": tactile.compute_force_field,
+        "penalty_forces": tactile.penalty_forces,
+        "net_wrench": tactile.net_wrench,
+        "query_sdf": geometry.query_sdf,
+    }[name]
+
+
+def patch(modules=None) -> list:
+    """Rebind the hot-path names in every importable reference module.
+    Returns the list of (module, name) pairs rebound."""
+    done = []
+    for mod_name, names in _SITES.items():
+        if modules is not None and mod_name not in modules:
+            continue
+        try:
+            mod = importlib.import_module(mod_name)
+        except Exception:  # noqa: BLE001 - module absent in this install
+            continue
+        for n in names:
+            if hasattr(mod, n):
+                _saved.setdefault((mod_name, n), getattr(mod, n))
+                setattr(mod, n, _impl(n))
+                done.append((mod_name, n))
+    return done
+
+
+def unpatch() -> None:
+    for (mod_name, n), fn in list(_saved.items()):
+        mod = importlib.import_module(mod_name)
+        setattr(mod, n, fn)
+    _saved.clear()

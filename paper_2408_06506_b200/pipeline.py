@@ -1,0 +1,124 @@
+"""Batched sensor step on one GPU: every (env, sensor) frame's tactile RGB,
+force field and net wrench from device-resident inputs.
+
+This is the multi-sensor caller of the two hot-path kernels -- the role of
+``PegEnvBatch._tactile_images`` / ``_tactile_ff`` (envs/peg_tasks.py:434-477)
+without their per-sensor Python loops: K1 runs once over all E*S depth maps
+and K2 once over all E*S force fields.  The two launches go to two streams so
+K2's float64 ALU work overlaps K1's HBM streaming; ``capture()`` records the
+pair in a CUDA graph so a step costs one graph launch.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device
+from .geometry import device_sdf
+from .render import depth_to_rgb_device, device_lut
+from .tactile import device_taxels, force_field_device
+
+
+class SensorArray:
+    def __init__(self, lut, sdf, points, params, n_envs, n_sensors=1, device=None, ff_fp64=False,
+                 rgb_u8=True, rgb_f32=False, overlap=True):
+        t = _device.torch()
+        self.device = _device.resolve_device(device)
+        self.lut = device_lut(lut)
+        self.sdf = device_sdf(sdf, self.device)
+        self.taxels = device_taxels(points, self.device)
+        self.rows, self.cols = int(points.rows), int(points.cols)
+        self.params = params
+        self.E, self.S = int(n_envs), int(n_sensors)
+        W, H = self.lut.image_size
+        self.H, self.W = H, W
+        dev = self.device
+        F = self.E * self.S
+        self.rgb_u8 = t.empty((self.E, self.S, H, W, 3), dtype=t.uint8, device=dev) if rgb_u8 else None
+        self.rgb_f32 = t.empty((self.E, self.S, H, W, 3), dtype=t.float32, device=dev) if rgb_f32 else None
+        ff_dtype = t.float64 if ff_fp64 else t.float32
+        self.f_n = t.empty((self.E, self.S, self.rows, self.cols, 3), dtype=ff_dtype, device=dev)
+        self.f_t = t.empty_like(self.f_n)
+        self.wrench = t.empty((self.E, self.S, 6), dtype=t.float64, device=dev)
+        self.overlap = overlap
+        self._ff_stream = t.cuda.Stream(device=dev) if overlap else None
+        self._graph = None
+        self._graph_inputs = None
+        assert F > 0
+
+    # bytes the step must move through HBM (our exact layout)
+    def algorithmic_bytes(self) -> dict:
+        px = self.H * self.W
+        rgb_out = (3 if self.rgb_u8 is not None else 0) + (12 if self.rgb_f32 is not None else 0)
+        taxel_out = self.rows * self.cols * 3 * self.f_n.element_size() * 2
+        F = self.E * self.S
+        rgb = F * px * (4 + rgb_out)
+        ff = F * (taxel_out + 13 * 8 + 6 * 8) + self.E * 13 * 8
+        return {"rgb": rgb, "ff": ff, "total": rgb + ff}
+
+    def launch(self, depth, obj_state, sen_state):
+        """Enqueue one step on the current stream (K2 on a forked stream that
+        joins back before returning)."""
+        t = _device.torch()
+        main = t.cuda.current_stream(self.device)
+        if self.overlap:
+            self._ff_stream.wait_stream(main)
+            with t.cuda.stream(self._ff_stream):
+                self._launch_ff(obj_state, sen_state)
+            self._launch_rgb(depth)
+            main.wait_stream(self._ff_stream)
+        else:
+            self._launch_rgb(depth)
+            self._launch_ff(obj_state, sen_state)
+
+    def _launch_rgb(self, depth):
+        depth_to_rgb_device(depth, self.lut, out_u8=self.rgb_u8, out_f32=self.rgb_f32)
+
+    def _launch_ff(self, obj_state, sen_state):
+        force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state, sen_state, self.params,
+                           self.f_n, self.f_t, wrench=self.wrench, n_sensors=self.S,
+                           obj_stride=13, sen_stride=13 * self.S)
+
+    def capture(self, depth, obj_state, sen_state):
+        """Record launch(depth, obj_state, sen_state) in a CUDA graph bound to
+        these input tensors; replay() then re-runs it with their current
+        contents."""
+        t = _device.torch()
+        s = t.cuda.Stream(device=self.device)
+        s.wait_stream(t.cuda.current_stream(self.device))
+        with t.cuda.stream(s):
+            self.launch(depth, obj_state, sen_state)  # warm-up outside capture (kernel attrs, lazy init)
+        t.cuda.current_stream(self.device).wait_stream(s)
+        t.cuda.synchronize(self.device)
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g):
+            self.launch(depth, obj_state, sen_state)
+        self._graph = g
+        self._graph_inputs = (depth, obj_state, sen_state)
+        return g
+
+    def replay(self):
+        self._graph.replay()
+
+    def step(self, depth, obj_state, sen_state):
+        if self._graph is not None and self._graph_inputs[0] is depth:
+            self.replay()
+        else:
+            self.launch(depth, obj_state, sen_state)
+        return self.rgb_u8 if self.rgb_u8 is not None else self.rgb_f32, self.f_n, self.f_t, self.wrench
+
+    # kernels launched per step (for the bench's gpu_launches count)
+    launches_per_step = 2
+
+
+def shard_range(n_envs: int, rank: int, world: int):
+    """Contiguous env shard [lo, hi) of `rank`."""
+    base, rem = divmod(n_envs, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def frame_checksum(rgb_u8, f_n, f_t) -> np.ndarray:
+    """Cheap per-shard digest for cross-rank validation: (sum of RGB bytes,
+    sum |f_n|, sum |f_t|) as float64."""
+    t = _device.torch()
+    return t.stack([rgb_u8.sum(dtype=t.float64), f_n.abs().sum(dtype=t.float64), f_t.abs().sum(dtype=t.float64)])

@@ -1,0 +1,197 @@
+"""Depth -> tactile RGB: drop-ins for ``gelsim.render`` hot-path functions.
+
+* ``depth_to_rgb(depth, lut)``   -- render/lut.py:68-76 (K1 on the GPU)
+* ``to_uint8(img)``              -- render/imageio.py:8-11
+* ``PolyLut``, ``DepthImage``, ``monomial_exponents``, ``synthetic_lut`` --
+  the data types / set-up of render/lut.py:20-59,165-181 and
+  render/depth.py:33-50.
+
+The computation always runs in libtacsl_b200.so on a B200; numpy inputs are
+copied to the device and results copied back, CUDA tensors stay on device.
+"""
+from __future__ import annotations
+
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device, _lib
+from .errors import LutResolutionMismatch
+
+
+def monomial_exponents(degree: int):
+    """(0,0), (1,0), (0,1), (2,0), (1,1), (0,2), ... (render/lut.py:20-22)."""
+    return [(s - j, j) for s in range(degree + 1) for j in range(s + 1)]
+
+
+@dataclass
+class DepthImage:
+    """(..., H, W) depth in metres along each camera ray (render/depth.py:33-50)."""
+
+    values: object
+    background: object
+
+    @property
+    def height(self) -> int:
+        return self.values.shape[-2]
+
+    @property
+    def width(self) -> int:
+        return self.values.shape[-1]
+
+    def indentation(self):
+        """Positive where the object indents past the membrane (depth.py:48-50)."""
+        if _device.is_cuda_tensor(self.values):
+            bg = _device.to_device(self.background, self.values.dtype, self.values.device)
+            return (bg - self.values).clamp_min(0.0)
+        return np.maximum(np.asarray(self.background) - np.asarray(self.values), 0.0)
+
+
+@dataclass
+class PolyLut:
+    """Per-channel polynomial over (g_x, g_y) up to a total degree (lut.py:31-59)."""
+
+    degree: int
+    coeffs: np.ndarray
+    image_size: tuple
+    sensor_id: str = ""
+    calibrated_on: str = ""
+    residual_rms: float = 0.0
+
+    def __post_init__(self):
+        if not (2 <= self.degree <= 4):
+            raise ValueError("LUT degree must be in [2, 4]")
+        n_terms = len(monomial_exponents(self.degree))
+        self.coeffs = np.asarray(self.coeffs, dtype=np.float64).reshape(3, n_terms)
+
+    @property
+    def background_color(self) -> np.ndarray:
+        return self.coeffs[:, 0].copy()
+
+
+def synthetic_lut(image_size, degree: int = 2, background=(0.35, 0.38, 0.45), seed: int = 0,
+                  gradient_scale: float = 1.0) -> PolyLut:
+    """The reference's demo table (lut.py:165-181): three directional linear
+    lobes of magnitude 3.5 plus uniform(-8, 8) higher-order terms drawn from
+    default_rng(seed) in (channel, term) order.  ``gradient_scale`` s
+    multiplies every (i, j) term by s**(i+j) -- the table for gradients
+    s times smaller (hard part 4)."""
+    rng = np.random.default_rng(seed)
+    exps = monomial_exponents(degree)
+    coeffs = np.zeros((3, len(exps)))
+    coeffs[:, 0] = background
+    lobes = ((1.0, 0.3), (-0.6, 0.8), (-0.4, -0.9))
+    for ch in range(3):
+        for k, (i, j) in enumerate(exps):
+            if i + j == 1:
+                coeffs[ch, k] = 3.5 * (lobes[ch][0] if i else lobes[ch][1])
+            elif i + j >= 2:
+                coeffs[ch, k] = rng.uniform(-8.0, 8.0)
+    if gradient_scale != 1.0:
+        for k, (i, j) in enumerate(exps):
+            coeffs[:, k] *= float(gradient_scale) ** (i + j)
+    return PolyLut(degree=degree, coeffs=coeffs, image_size=tuple(image_size))
+
+
+class DeviceLut:
+    """A LUT handle of libtacsl_b200 (coefficients travel as kernel parameters)."""
+
+    def __init__(self, lut):
+        lib = _lib.load()
+        coeffs = np.ascontiguousarray(np.asarray(lut.coeffs, dtype=np.float64))
+        W, H = (int(v) for v in lut.image_size)
+        handle = _lib.c_void_p()
+        _lib.check(lib.tacsl_lut_create(coeffs.ctypes.data, int(lut.degree), W, H, _lib.ctypes.byref(handle)))
+        self.handle = handle
+        self.degree = int(lut.degree)
+        self.image_size = (W, H)
+        self._finalizer = weakref.finalize(self, lib.tacsl_lut_destroy, handle)
+
+
+_lut_lock = threading.Lock()
+_lut_cache: dict = {}
+
+
+def device_lut(lut) -> DeviceLut:
+    if isinstance(lut, DeviceLut):
+        return lut
+    coeffs = np.asarray(lut.coeffs, dtype=np.float64)
+    key = (int(lut.degree), tuple(int(v) for v in lut.image_size), coeffs.tobytes())
+    with _lut_lock:
+        h = _lut_cache.get(key)
+        if h is None:
+            h = DeviceLut(lut)
+            if len(_lut_cache) > 64:
+                _lut_cache.clear()
+            _lut_cache[key] = h
+    return h
+
+
+def _values(depth):
+    return depth.values if hasattr(depth, "values") else depth
+
+
+def depth_to_rgb_device(depth_values, lut, out_u8=None, out_f32=None, stream=None):
+    """Device-level K1: (..., H, W) float32 CUDA tensor -> (..., H, W, 3)
+    uint8 and/or float32 CUDA tensors (pre-allocated or allocated here)."""
+    t = _device.torch()
+    dl = device_lut(lut)
+    v = depth_values
+    if not (_device.is_cuda_tensor(v) and v.dtype == t.float32 and v.is_contiguous()):
+        raise TypeError("depth_to_rgb_device wants a contiguous float32 CUDA tensor")
+    H, W = v.shape[-2], v.shape[-1]
+    n = int(np.prod(v.shape[:-2], dtype=np.int64)) if v.ndim > 2 else 1
+    lib = _lib.load()
+    sh = _device.stream_handle(v.device) if stream is None else stream
+    _lib.check(lib.tacsl_depth_to_rgb(dl.handle, v.data_ptr(), n, H, W, _device.ptr(out_u8),
+                                      _device.ptr(out_f32), sh))
+    return out_u8, out_f32
+
+
+def depth_to_rgb(depth, lut, out_dtype=None):
+    """Drop-in for gelsim.render.depth_to_rgb (render/lut.py:68-76).
+
+    Returns the (..., H, W, 3) image in [0, 1]: float64 numpy for numpy input
+    (the reference's dtype), float32 CUDA tensor for CUDA input.  With
+    ``out_dtype=np.uint8`` (or torch.uint8) the to_uint8 quantisation
+    (imageio.py:8-11) is fused into the same kernel.
+    Raises LutResolutionMismatch when (W, H) != lut.image_size (lut.py:70-74).
+    """
+    t = _device.torch()
+    values = _values(depth)
+    W, H = values.shape[-1], values.shape[-2]
+    if (W, H) != tuple(lut.image_size):
+        raise LutResolutionMismatch(f"LUT calibrated at {tuple(lut.image_size)}, image is {(W, H)}")
+    on_device = _device.is_cuda_tensor(values)
+    dev = _device.resolve_device(values.device if on_device else None)
+    v = _device.to_device(values, t.float32, dev)
+    want_u8 = out_dtype in (np.uint8, t.uint8, "uint8")
+    shape = tuple(v.shape) + (3,)
+    if want_u8:
+        out = t.empty(shape, dtype=t.uint8, device=dev)
+        depth_to_rgb_device(v, lut, out_u8=out)
+    else:
+        out = t.empty(shape, dtype=t.float32, device=dev)
+        depth_to_rgb_device(v, lut, out_f32=out)
+    if on_device:
+        return out
+    host = out.cpu().numpy()
+    return host if want_u8 else host.astype(np.float64)
+
+
+def to_uint8(img):
+    """Drop-in for gelsim.render.to_uint8 (imageio.py:8-11): clip(rint(255 x)).
+    uint8 input is returned as is; float input is quantised on the GPU."""
+    t = _device.torch()
+    if isinstance(img, np.ndarray) and img.dtype == np.uint8:
+        return img
+    if _device.is_cuda_tensor(img) and img.dtype == t.uint8:
+        return img
+    on_device = _device.is_cuda_tensor(img)
+    dev = _device.resolve_device(img.device if on_device else None)
+    x = _device.to_device(img, t.float32, dev)
+    out = t.empty(x.shape, dtype=t.uint8, device=dev)
+    _lib.check(_lib.load().tacsl_to_uint8(x.data_ptr(), x.numel(), out.data_ptr(), _device.stream_handle(dev)))
+    return out if on_device else out.cpu().numpy()

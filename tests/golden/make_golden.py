@@ -1,0 +1,178 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+    python tests/golden/make_golden.py
+
+Imports the reference package ``gelsim`` read-only from
+/root/reference/pkg/src (this container only -- /root/reference does not
+exist on the GPU box) and records inputs + reference outputs of every
+hot-path function into tests/golden/*.npz.  The committed .npz files are
+what the tests read; this script is kept so the fixtures can be re-made.
+
+Fixtures:
+  rgb.npz        depth_to_rgb (+ to_uint8) at 60x80 (degrees 2-4, scaled and
+                 unscaled LUTs), 240x320 (uint8), odd sizes, and the
+                 reference tests' flat / tilted / clamp cases
+  sdf.npz        query_sdf on a reference-built (build_sdf) peg grid
+  ff.npz         compute_force_field (+ kinematics) and net_wrench for a
+                 batch of random peg presses with random sensor poses,
+                 plus one unbatched call
+  penalty.npz    penalty_forces on the seed-11 draws of
+                 test_tactile_field.py:153-168
+"""
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+REF_SRC = Path("/root/reference/pkg/src")
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
+sys.path.insert(0, str(REF_SRC))
+sys.path.insert(0, str(ROOT))
+
+from gelsim.geometry import build_sdf, make_cylinder, query_sdf  # noqa: E402
+from gelsim.render import DepthImage, PolyLut, depth_to_rgb, synthetic_lut, to_uint8  # noqa: E402
+from gelsim.sensors import TactileSensorSpec  # noqa: E402
+from gelsim.tactile import PenaltyParams, compute_force_field, net_wrench, penalty_forces  # noqa: E402
+from gelsim.tactile import sample_tactile_points  # noqa: E402
+
+from paper_2408_06506_b200 import synthetic  # noqa: E402  (input generators only)
+from paper_2408_06506_b200.sensors import camera_for_sensor as my_camera  # noqa: E402
+from paper_2408_06506_b200.sensors import reference_depth as my_background  # noqa: E402
+
+
+def scaled_lut(image_size, degree, seed=0, s=1.0):
+    lut = synthetic_lut(image_size, degree=degree, seed=seed)
+    coeffs = lut.coeffs.copy()
+    k = 0
+    for tot in range(degree + 1):
+        for j in range(tot + 1):
+            coeffs[:, k] *= s ** tot
+            k += 1
+    return PolyLut(degree=degree, coeffs=coeffs, image_size=tuple(image_size))
+
+
+def depth_maps(W, H, n, config_id):
+    sensor = TactileSensorSpec(image_size=(W, H))
+    cam = my_camera(sensor)
+    bg = my_background(cam, sensor)
+    return synthetic.depth_batch(cam, bg, n, config_id=config_id), bg
+
+
+def make_rgb():
+    out = {}
+    # 60x80 (reference default camera), scaled LUTs, degrees 2..4
+    d, bg = depth_maps(80, 60, 3, config_id=101)
+    out["d60"] = d
+    for deg in (2, 3, 4):
+        lut = scaled_lut((80, 60), deg, seed=deg, s=synthetic.lut_scale((80, 60)))
+        rgb = depth_to_rgb(DepthImage(values=d.astype(np.float64), background=bg), lut)
+        out[f"c60_deg{deg}"] = lut.coeffs
+        out[f"rgb60_deg{deg}"] = rgb
+        out[f"u8_60_deg{deg}"] = to_uint8(rgb)
+    # unscaled reference demo LUT (flat-looking images)
+    lut = synthetic_lut((80, 60), degree=2, seed=0)
+    out["c60_plain"] = lut.coeffs
+    out["rgb60_plain"] = depth_to_rgb(DepthImage(values=d.astype(np.float64), background=bg), lut)
+    # 240x320, uint8 only (degree 2, the env default)
+    d2, bg2 = depth_maps(320, 240, 1, config_id=102)
+    lut = scaled_lut((320, 240), 2, seed=0, s=synthetic.lut_scale((320, 240)))
+    out["d240"] = d2
+    out["c240"] = lut.coeffs
+    out["u8_240"] = to_uint8(depth_to_rgb(DepthImage(values=d2.astype(np.float64), background=bg2), lut))
+    # odd sizes (misaligned rows: generic kernel path)
+    rng = np.random.default_rng(5)
+    for (H, W) in ((2, 3), (5, 7), (9, 18), (3, 2)):
+        v = (0.02 + rng.uniform(-1e-4, 1e-4, (2, H, W))).astype(np.float32)
+        lut = scaled_lut((W, H), 3, seed=1, s=300.0)
+        out[f"odd_{H}x{W}_d"] = v
+        out[f"odd_{H}x{W}_c"] = lut.coeffs
+        out[f"odd_{H}x{W}_rgb"] = depth_to_rgb(DepthImage(values=v.astype(np.float64), background=v[0]), lut)
+    # reference tests' analytic cases (test_render.py:108-138)
+    tilt = np.zeros((3, 6))
+    tilt[:, 0] = 0.5
+    tilt[0, 1] = 1.0
+    xs = (np.arange(80) * 1e-4).astype(np.float32)
+    v = np.broadcast_to(xs, (60, 80)).copy()
+    out["tilt_d"] = v
+    out["tilt_c"] = tilt
+    out["tilt_rgb"] = depth_to_rgb(DepthImage(values=v.astype(np.float64), background=v),
+                                   PolyLut(degree=2, coeffs=tilt, image_size=(80, 60)))
+    xs = (np.arange(80) * 10.0).astype(np.float32)
+    v = np.broadcast_to(xs, (60, 80)).copy()
+    out["clamp_d"] = v
+    out["clamp_rgb"] = depth_to_rgb(DepthImage(values=v.astype(np.float64), background=v),
+                                    PolyLut(degree=2, coeffs=tilt, image_size=(80, 60)))
+    np.savez_compressed(HERE / "rgb.npz", **out)
+
+
+def peg_grid_reference():
+    # small dims keep the fixture at ~0.25 MB; float64 values as build_sdf makes them
+    return build_sdf(make_cylinder(0.008, 0.05, segments=32), dims=(16, 16, 32), padding=0.004)
+
+
+def make_sdf(grid):
+    rng = np.random.default_rng(7)
+    lo, hi = grid.origin, grid.upper
+    span = hi - lo
+    pts = lo - 0.1 * span + rng.uniform(0, 1.2, (3000, 3)) * span   # ~half outside on some axis
+    inside = lo + rng.uniform(0, 1, (2000, 3)) * span
+    # exact boundary / corner points (rel == 0 and rel == dims-1)
+    corners = np.array([lo, hi, [lo[0], hi[1], lo[2]], [hi[0], lo[1], hi[2]]])
+    pts = np.concatenate([pts, inside, corners])
+    q = query_sdf(grid, pts)
+    np.savez_compressed(HERE / "sdf.npz", origin=grid.origin, spacing=grid.spacing, dims=np.array(grid.dims),
+                        values=grid.values, gradients=grid.gradients, points=pts,
+                        distance=q.distance, normal=q.normal, valid=q.valid)
+
+
+def make_ff(grid):
+    sensor = TactileSensorSpec(image_size=(320, 240))
+    pts = sample_tactile_points(sensor, 20, 25)
+    obj, sen = synthetic.peg_states(12, 1, config_id=103, random_sensor_pose=True)
+    sen = sen[:, 0]
+    params = PenaltyParams()
+    fld, kin = compute_force_field(pts, grid, obj[:, 0:3], obj[:, 3:7], obj[:, 7:10], obj[:, 10:13],
+                                   sen[:, 0:3], sen[:, 3:7], sen[:, 7:10], sen[:, 10:13], params,
+                                   return_kinematics=True)
+    force, torque = net_wrench(fld, pts)
+    # one unbatched call (sensor at identity, object relative pose of env 0)
+    o1, s1 = synthetic.peg_states(1, 1, config_id=104, random_sensor_pose=False)
+    p2 = PenaltyParams(k_n=850.0, k_d=40.0, k_t=7.0, mu=1.3)
+    fld1 = compute_force_field(pts, grid, o1[0, 0:3], o1[0, 3:7], o1[0, 7:10], o1[0, 10:13],
+                               s1[0, 0, 0:3], s1[0, 0, 3:7], s1[0, 0, 7:10], s1[0, 0, 10:13], p2)
+    np.savez_compressed(HERE / "ff.npz", points=pts.points, obj=obj, sen=sen,
+                        f_n=fld.f_n, f_t=fld.f_t, d=kin["d"], d_dot=kin["d_dot"], v_t=kin["v_t"], n=kin["n"],
+                        force=force, torque=torque, obj1=o1[0], sen1=s1[0, 0], params1=np.array(
+                            [p2.k_n, p2.k_d, p2.k_t, p2.mu]), f_n1=fld1.f_n, f_t1=fld1.f_t)
+
+
+def make_penalty():
+    rng = np.random.default_rng(11)
+    n_pts = 10000
+    d = rng.uniform(-2e-3, 1e-3, n_pts)
+    d_dot = rng.uniform(-0.5, 0.5, n_pts)
+    n = rng.normal(size=(n_pts, 3))
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    v_t = rng.normal(size=(n_pts, 3)) * 0.05
+    params = PenaltyParams(k_n=850.0, k_d=40.0, k_t=7.0, mu=1.3)
+    f_n, f_t = penalty_forces(d, d_dot, n, v_t, params)
+    sel = slice(0, 3000)
+    np.savez_compressed(HERE / "penalty.npz", d=d[sel], d_dot=d_dot[sel], n=n[sel], v_t=v_t[sel],
+                        params=np.array([params.k_n, params.k_d, params.k_t, params.mu]),
+                        f_n=f_n[sel], f_t=f_t[sel])
+
+
+if __name__ == "__main__":
+    make_rgb()
+    g = peg_grid_reference()
+    make_sdf(g)
+    make_ff(g)
+    make_penalty()
+    for p in sorted(HERE.glob("*.npz")):
+        print(p.name, p.stat().st_size)

@@ -1,0 +1,257 @@
+"""K2 (force field + wrench), query_sdf and penalty_forces parity on the GPU.
+
+Contract (BASELINE.json north_star): force fields within 1e-5 relative;
+taxel indexing and contact masks bit-exact.  The kernel's float64 mask chain
+reproduces the reference's distance bit for bit, so the tests also assert
+d == d_ref exactly."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import sdf_tuple, vec_close
+from oracle import gelsim_oracle as O
+from paper_2408_06506_b200 import geometry, synthetic, tactile
+from paper_2408_06506_b200.errors import DimensionMismatch
+from paper_2408_06506_b200.geometry import query_sdf
+from paper_2408_06506_b200.sensors import IDENTITY_QUAT, TactileSensorSpec
+from paper_2408_06506_b200.tactile import (
+    ForceField,
+    PenaltyParams,
+    TactilePointGrid,
+    compute_force_field,
+    net_wrench,
+    penalty_forces,
+    sample_tactile_points,
+)
+
+pytestmark = pytest.mark.gpu
+
+FF_RTOL = 1e-5
+
+STILL = dict(object_linvel=np.zeros(3), object_angvel=np.zeros(3), sensor_pos=np.zeros(3),
+             sensor_quat=IDENTITY_QUAT, sensor_linvel=np.zeros(3), sensor_angvel=np.zeros(3))
+
+
+@pytest.fixture(scope="module")
+def plate_sdf():
+    return geometry.box_grid((0.1, 0.1, 0.02), dims=(48, 48, 24), padding=0.01)
+
+
+def sensor_grid(rows=10, cols=10):
+    return sample_tactile_points(TactileSensorSpec(), rows, cols)
+
+
+# ------------------------------------------------------------------ golden ---
+
+def test_query_sdf_golden_bit_exact(golden, golden_grid):
+    z = golden("sdf")
+    q = query_sdf(golden_grid, z["points"])
+    assert np.array_equal(q.valid, z["valid"])
+    assert np.array_equal(q.distance, z["distance"])
+    np.testing.assert_allclose(q.normal, z["normal"], rtol=0, atol=1e-14)
+    single = query_sdf(golden_grid, z["points"][3000])
+    assert single.distance == z["distance"][3000] and bool(single.valid) == bool(z["valid"][3000])
+
+
+def test_force_field_golden(golden, golden_grid):
+    z = golden("ff")
+    obj, sen = z["obj"], z["sen"]
+    pts = TactilePointGrid(points=z["points"], rest_normals=np.zeros_like(z["points"]), spacing=(1e-3, 1e-3))
+    fld, kin = compute_force_field(pts, golden_grid, obj[:, 0:3], obj[:, 3:7], obj[:, 7:10], obj[:, 10:13],
+                                   sen[:, 0:3], sen[:, 3:7], sen[:, 7:10], sen[:, 10:13], PenaltyParams(),
+                                   return_kinematics=True)
+    assert np.array_equal(kin["d"], z["d"])                    # distance bit-exact (=> mask bit-exact)
+    assert np.array_equal(kin["d"] < 0, z["d"] < 0)
+    ok, worst = vec_close(fld.f_n, z["f_n"], FF_RTOL)
+    assert ok, worst
+    ok, worst = vec_close(fld.f_t, z["f_t"], FF_RTOL)
+    assert ok, worst
+    # achieved precision is far inside the contract
+    assert vec_close(fld.f_n, z["f_n"], 1e-11)[0] and vec_close(fld.f_t, z["f_t"], 1e-9)[0]
+    np.testing.assert_allclose(kin["n"], z["n"], atol=1e-13)
+    np.testing.assert_allclose(kin["d_dot"], z["d_dot"], atol=1e-14)
+    force, torque = net_wrench(fld, pts)
+    np.testing.assert_allclose(force, z["force"], rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(torque, z["torque"], rtol=1e-8, atol=1e-15)
+
+
+def test_force_field_unbatched_golden(golden, golden_grid):
+    z = golden("ff")
+    o, s, p = z["obj1"], z["sen1"], z["params1"]
+    pts = TactilePointGrid(points=z["points"], rest_normals=np.zeros_like(z["points"]), spacing=(1e-3, 1e-3))
+    fld = compute_force_field(pts, golden_grid, o[0:3], o[3:7], o[7:10], o[10:13], s[0:3], s[3:7], s[7:10],
+                              s[10:13], PenaltyParams(*p))
+    assert fld.f_n.shape == (20, 25, 3)
+    assert vec_close(fld.f_n, z["f_n1"], FF_RTOL)[0]
+    assert vec_close(fld.f_t, z["f_t1"], FF_RTOL)[0]
+
+
+def test_penalty_forces_golden_and_scalar(golden):
+    z = golden("penalty")
+    f_n, f_t = penalty_forces(z["d"], z["d_dot"], z["n"], z["v_t"], PenaltyParams(*z["params"]))
+    np.testing.assert_allclose(f_n, z["f_n"], atol=1e-12)
+    np.testing.assert_allclose(f_t, z["f_t"], atol=1e-12)
+
+
+# ------------------------------------------------------- oracle, larger ------
+
+@pytest.mark.parametrize("ff_grid", [(20, 25), (80, 100)])
+def test_force_field_vs_oracle_random_sensor_poses(ff_grid):
+    sdf = synthetic.peg_grid((32, 32, 64))
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), *ff_grid)
+    E = 64 if ff_grid == (20, 25) else 8
+    obj, sen = synthetic.peg_states(E, 1, config_id=21, random_sensor_pose=True)
+    sen = sen[:, 0]
+    params = PenaltyParams()
+    fld, kin = compute_force_field(pts, sdf, obj[:, 0:3], obj[:, 3:7], obj[:, 7:10], obj[:, 10:13],
+                                   sen[:, 0:3], sen[:, 3:7], sen[:, 7:10], sen[:, 10:13], params,
+                                   return_kinematics=True)
+    f_n, f_t, rk = O.compute_force_field(pts.points, *sdf_tuple(sdf), obj[:, 0:3], obj[:, 3:7], obj[:, 7:10],
+                                         obj[:, 10:13], sen[:, 0:3], sen[:, 3:7], sen[:, 7:10], sen[:, 10:13])
+    contact = rk["d"] < 0
+    assert 0.05 < contact.mean() < 0.6                          # non-vacuous
+    assert np.array_equal(kin["d"], rk["d"])
+    assert vec_close(fld.f_n, f_n, FF_RTOL)[0]
+    assert vec_close(fld.f_t, f_t, FF_RTOL)[0]
+
+
+def test_device_path_fp32_two_sensors_mask_and_wrench():
+    t = torch
+    sdf = synthetic.peg_grid((32, 32, 64))
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 20, 25)
+    E, S = 48, 2
+    obj, sen = synthetic.peg_states(E, S, config_id=22)
+    dev = t.device("cuda")
+    tax = tactile.device_taxels(pts, dev)
+    o = t.from_numpy(obj).to(dev)
+    s = t.from_numpy(np.ascontiguousarray(sen)).to(dev)
+    f_n = t.empty((E, S, 20, 25, 3), dtype=t.float32, device=dev)
+    f_t = t.empty_like(f_n)
+    wrench = t.empty((E, S, 6), dtype=t.float64, device=dev)
+    contact = t.empty((E, S, 20, 25), dtype=t.uint8, device=dev)
+    tactile.force_field_device(sdf, tax, 20, 25, o, s, PenaltyParams(), f_n, f_t, wrench=wrench,
+                               contact=contact, n_sensors=S)
+    t.cuda.synchronize()
+    objE = np.repeat(obj, S, axis=0)
+    senE = sen.reshape(E * S, 13)
+    rn, rt, rk = O.compute_force_field(pts.points, *sdf_tuple(sdf), objE[:, 0:3], objE[:, 3:7], objE[:, 7:10],
+                                       objE[:, 10:13], senE[:, 0:3], senE[:, 3:7], senE[:, 7:10], senE[:, 10:13])
+    assert np.array_equal(contact.cpu().numpy().reshape(E * S, 20, 25).astype(bool), rk["d"] < 0)
+    assert vec_close(f_n.cpu().numpy().reshape(E * S, 20, 25, 3), rn, FF_RTOL, atol=1e-9)[0]
+    assert vec_close(f_t.cpu().numpy().reshape(E * S, 20, 25, 3), rt, FF_RTOL, atol=1e-9)[0]
+    force, torque = O.net_wrench(rn, rt, pts.points)
+    w = wrench.cpu().numpy().reshape(E * S, 6)
+    scale = np.abs(rn + rt).sum(axis=(1, 2))       # sum of |f| bounds the cancellation
+    assert np.all(np.abs(w[:, 0:3] - force) <= 1e-12 * scale + 1e-15)
+    assert np.all(np.abs(w[:, 3:6] - torque) <= 1e-12 * scale * 0.02 + 1e-15)
+
+
+# ----------------------------------------- reference tests, re-pinned on GPU --
+# (pkg/tests/test_tactile_field.py)
+
+def test_no_penetration_zero_field(plate_sdf):
+    fld = compute_force_field(sensor_grid(), plate_sdf, object_pos=np.array([0, 0, 0.02]),
+                              object_quat=IDENTITY_QUAT, params=PenaltyParams(), **STILL)
+    assert np.all(fld.f_n == 0) and np.all(fld.f_t == 0)
+
+
+def test_static_press_normal_magnitude(plate_sdf):
+    params = PenaltyParams(k_n=1000.0, k_d=0.0, k_t=10.0, mu=2.0)
+    fld = compute_force_field(sensor_grid(), plate_sdf, object_pos=np.array([0, 0, 0.01 - 0.001]),
+                              object_quat=IDENTITY_QUAT, params=params, **STILL)
+    mags = np.linalg.norm(fld.f_n, axis=-1)
+    np.testing.assert_allclose(mags, 1.0, rtol=1e-6)
+
+
+def test_sliding_press_hits_cone_boundary(plate_sdf):
+    params = PenaltyParams(k_n=1000.0, k_d=0.0, k_t=1e4, mu=1.0)
+    kw = dict(STILL)
+    kw["sensor_linvel"] = np.array([0.01, 0.0, 0.0])
+    fld = compute_force_field(sensor_grid(), plate_sdf, object_pos=np.array([0, 0, 0.01 - 0.001]),
+                              object_quat=IDENTITY_QUAT, params=params, **kw)
+    expected = np.zeros((10, 10, 3))
+    expected[..., 0] = -1.0
+    np.testing.assert_allclose(fld.f_t, expected, atol=1e-9)
+
+
+def test_batched_matches_single_bit_exact(plate_sdf):
+    params = PenaltyParams()
+    pos = np.array([[0, 0, 0.0095], [0, 0, 0.0090], [0, 0, 0.02]])
+    quat = np.tile(IDENTITY_QUAT, (3, 1))
+    fld = compute_force_field(sensor_grid(), plate_sdf, pos, quat, np.zeros((3, 3)), np.zeros((3, 3)),
+                              np.zeros((3, 3)), quat, np.zeros((3, 3)), np.zeros((3, 3)), params)
+    for e in range(3):
+        solo = compute_force_field(sensor_grid(), plate_sdf, pos[e], IDENTITY_QUAT, params=params, **STILL)
+        assert np.array_equal(fld.f_n[e], solo.f_n)
+        assert np.array_equal(fld.f_t[e], solo.f_t)
+
+
+def test_cone_and_directionality_random_sweep():
+    rng = np.random.default_rng(12)
+    n_pts = 10000
+    d = rng.uniform(-3e-3, 5e-4, n_pts)
+    d_dot = rng.uniform(-1, 1, n_pts)
+    n = rng.normal(size=(n_pts, 3))
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    v_t = rng.normal(size=(n_pts, 3)) * rng.uniform(0, 0.2, (n_pts, 1))
+    params = PenaltyParams(k_n=1200.0, k_d=90.0, k_t=15.0, mu=0.9)
+    f_n, f_t = penalty_forces(d, d_dot, n, v_t, params)
+    fn_mag = np.linalg.norm(f_n, axis=-1)
+    ft_mag = np.linalg.norm(f_t, axis=-1)
+    assert np.all(ft_mag <= params.mu * fn_mag + 1e-9)
+    assert np.all(np.einsum("ij,ij->i", f_t, v_t) <= 0)
+    assert np.all(np.einsum("ij,ij->i", f_n, n) >= 0)
+
+
+def test_repulsion_clamp_when_separating_fast():
+    f_n, f_t = penalty_forces(-1e-3, 50.0, np.array([0, 0, 1.0]), np.zeros(3), PenaltyParams(k_n=100.0, k_d=10.0))
+    assert np.all(f_n == 0) and np.all(f_t == 0)
+
+
+def test_resolution_consistency_after_density_normalization():
+    r = 0.02
+    big_sphere = geometry.sphere_grid(r, dims=(64, 64, 64), padding=0.004)
+    params = PenaltyParams()
+    wrenches = {}
+    for res in (10, 100):
+        grid = sample_tactile_points(TactileSensorSpec(), res, res)
+        fld = compute_force_field(grid, big_sphere, object_pos=np.array([0, 0, r - 0.0015]),
+                                  object_quat=IDENTITY_QUAT, params=params, **STILL)
+        force, _ = net_wrench(fld, grid)
+        wrenches[res] = force * grid.spacing[0] * grid.spacing[1]
+    assert np.linalg.norm(wrenches[10] - wrenches[100]) / np.linalg.norm(wrenches[100]) < 0.05
+
+
+def test_symmetric_press_zero_torque(plate_sdf):
+    grid = sensor_grid()
+    fld = compute_force_field(grid, plate_sdf, object_pos=np.array([0, 0, 0.01 - 0.0005]),
+                              object_quat=IDENTITY_QUAT, params=PenaltyParams(), **STILL)
+    force, torque = net_wrench(fld, grid)
+    assert np.linalg.norm(torque) < 1e-9 * np.linalg.norm(force) * 0.024 + 1e-15
+
+
+def test_two_point_wrench_hand_sum():
+    pts = np.zeros((1, 2, 3))
+    pts[0, 0, 0] = 0.01
+    pts[0, 1, 0] = -0.01
+    grid = TactilePointGrid(points=pts, rest_normals=np.zeros((1, 2, 3)), spacing=(0.02, 0.02))
+    f_n = np.zeros((1, 2, 3))
+    f_n[..., 2] = 1.0
+    force, torque = net_wrench(ForceField(f_n=f_n, f_t=np.zeros((1, 2, 3))), grid)
+    np.testing.assert_allclose(force, [0, 0, 2.0])
+    np.testing.assert_allclose(torque, [0, 0, 0], atol=1e-15)
+
+
+def test_wrench_dimension_mismatch():
+    with pytest.raises(DimensionMismatch):
+        net_wrench(ForceField(f_n=np.zeros((5, 5, 3)), f_t=np.zeros((5, 5, 3))), sensor_grid(10, 10))
+
+
+def test_query_sdf_sentinel_and_device_tensors():
+    g = geometry.sphere_grid(0.005, dims=(32, 32, 32))
+    pts = np.array([[0.0, 0.0, 0.0], [1.0, 1.0, 1.0], [0.0, 0.0, 0.004]])
+    q = query_sdf(g, pts)
+    assert list(q.valid) == [True, False, True]
+    assert np.isinf(q.distance[1]) and np.all(q.normal[1] == 0)
+    qd = query_sdf(g, torch.from_numpy(pts).cuda())
+    assert torch.equal(qd.distance.cpu(), torch.from_numpy(q.distance))

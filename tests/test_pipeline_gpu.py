@@ -1,0 +1,77 @@
+"""The batched sensor step (SensorArray): RGB + force field + wrench for
+E envs x S sensors in two overlapped launches, eager and CUDA-graph replay,
+against the CPU oracle."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import sdf_tuple, vec_close
+from oracle import gelsim_oracle as O
+from paper_2408_06506_b200 import SensorArray, synthetic
+from paper_2408_06506_b200.tactile import PenaltyParams
+
+pytestmark = pytest.mark.gpu
+
+
+def setup(E=6, S=2, image=(320, 240)):
+    _, cam, bg, lut, pts = synthetic.sensor_setup(image, (20, 25))
+    sdf = synthetic.peg_grid((32, 32, 64))
+    depth = synthetic.depth_batch(cam, bg, E * S, config_id=31).reshape(E, S, image[1], image[0])
+    obj, sen = synthetic.peg_states(E, S, config_id=31)
+    return lut, pts, sdf, depth, obj, sen
+
+
+def oracle_step(lut, pts, sdf, depth, obj, sen):
+    E, S = sen.shape[:2]
+    objE = np.repeat(obj, S, axis=0)
+    senE = sen.reshape(E * S, 13)
+    rgb, f_n, f_t, force, torque = O.sensor_frames(depth.reshape((E * S,) + depth.shape[2:]), lut.coeffs,
+                                                   lut.degree, pts.points, sdf_tuple(sdf), objE, senE,
+                                                   (1000.0, 100.0, 10.0, 2.0))
+    return rgb, f_n, f_t, force, torque
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_sensor_array_step_vs_oracle(overlap):
+    lut, pts, sdf, depth, obj, sen = setup()
+    E, S = sen.shape[:2]
+    arr = SensorArray(lut, sdf, pts, PenaltyParams(), E, S, overlap=overlap)
+    d = torch.from_numpy(depth).cuda()
+    o = torch.from_numpy(obj).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(sen)).cuda()
+    rgb, f_n, f_t, wrench = arr.step(d, o, s)
+    torch.cuda.synchronize()
+    r_rgb, r_fn, r_ft, r_force, r_torque = oracle_step(lut, pts, sdf, depth, obj, sen)
+    diff = np.abs(rgb.cpu().numpy().reshape(r_rgb.shape).astype(int) - r_rgb.astype(int))
+    assert diff.max() <= 1
+    assert vec_close(f_n.cpu().numpy().reshape(r_fn.shape), r_fn, 1e-5, atol=1e-9)[0]
+    assert vec_close(f_t.cpu().numpy().reshape(r_ft.shape), r_ft, 1e-5, atol=1e-9)[0]
+    w = wrench.cpu().numpy().reshape(E * S, 6)
+    np.testing.assert_allclose(w[:, :3], r_force, rtol=1e-9, atol=1e-12)
+
+
+def test_cuda_graph_replay_matches_eager():
+    lut, pts, sdf, depth, obj, sen = setup(E=16)
+    E, S = sen.shape[:2]
+    arr = SensorArray(lut, sdf, pts, PenaltyParams(), E, S)
+    d = torch.from_numpy(depth).cuda()
+    o = torch.from_numpy(obj).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(sen)).cuda()
+    arr.launch(d, o, s)
+    torch.cuda.synchronize()
+    eager = [x.clone() for x in (arr.rgb_u8, arr.f_n, arr.f_t, arr.wrench)]
+    arr.capture(d, o, s)
+    for x in (arr.rgb_u8, arr.f_n, arr.f_t, arr.wrench):
+        x.zero_()
+    # new inputs in the captured buffers are picked up by replay
+    d2 = torch.from_numpy(np.ascontiguousarray(depth[::-1])).cuda()
+    d.copy_(d2)
+    arr.replay()
+    torch.cuda.synchronize()
+    rgb_rev = arr.rgb_u8.clone()
+    d.copy_(torch.from_numpy(depth).cuda())
+    arr.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, (arr.rgb_u8, arr.f_n, arr.f_t, arr.wrench)):
+        assert torch.equal(a, b)
+    assert torch.equal(rgb_rev, eager[0].flip(0))

@@ -45,6 +45,8 @@ def to_device(x, dtype, device):
         return x.to(device=device, dtype=dtype).contiguous()
     np_dtype = {t.float32: np.float32, t.float64: np.float64, t.uint8: np.uint8}[dtype]
     arr = np.ascontiguousarray(np.asarray(x, dtype=np_dtype))
+    if not arr.flags.writeable:
+        arr = arr.copy()
     return t.from_numpy(arr).to(device)
 
 

@@ -130,7 +130,10 @@ def device_lut(lut) -> DeviceLut:
 
 
 def _values(depth):
-    return depth.values if hasattr(depth, "values") else depth
+    """DepthImage (ours or the reference's) -> its values; arrays/tensors pass."""
+    if isinstance(depth, np.ndarray) or _device.is_cuda_tensor(depth) or not hasattr(depth, "values"):
+        return depth
+    return depth.values
 
 
 def depth_to_rgb_device(depth_values, lut, out_u8=None, out_f32=None, stream=None):

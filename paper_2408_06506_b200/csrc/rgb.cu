@@ -7,15 +7,19 @@
 //
 // Layout: depth (N, H, W) fp32, rgb (N, H, W, 3) HWC, u8 and/or fp32.
 //
-// Fast path (W % 4 == 0, 16B-aligned pointers): persistent CTAs walk work
-// units = (image, band of B rows).  Thread 0 streams each band plus its two
-// halo rows global->shared with one bulk-async copy (cp.async.bulk, the 1-D
-// TMA engine) into a STAGES-deep ring completed on mbarriers, so up to
-// STAGES bands per CTA are in flight while the CTA shades the current one.
-// Every thread shades 4 adjacent pixels (one 16B shared-memory vector +
-// neighbours), writes 12 output bytes into a shared staging tile, and the
-// band's contiguous B*W*3 bytes go back with one bulk shared->global store.
-// HBM sees each depth byte read once and each RGB byte written once.
+// Fast path (W % 4 == 0, W <= 1536, 16B-aligned pointers): persistent CTAs
+// walk work units = (image, band of B rows).  Thread 0 streams each band
+// plus its two halo rows global->shared with ONE bulk-async copy
+// (cp.async.bulk, the 1-D TMA engine) into a STAGES-deep ring completed on
+// mbarriers, so several bands per CTA are in flight while the CTA shades
+// the current one.  Thread (g, xq) owns column quad xq (4 pixels) and walks
+// RPT consecutive rows of row-group g, rolling the up/centre/down rows in
+// registers (one 16B shared load per row).  Pixels are shaded in pairs with
+// the Blackwell packed-fp32 pipe (FFMA2/FADD2: two pixels per instruction);
+// only the last Horner step is scalar, to get the free .SAT clamp.  The
+// uint8 bytes are packed with PRMT into a shared staging tile and the band's
+// contiguous B*W*3 bytes leave with one bulk shared->global store.  HBM sees
+// each depth byte read once and each RGB byte written once.
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -26,7 +30,8 @@
 namespace tacsl {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kMaxThreads = 384;  // with 2 CTAs/SM: <= 85 registers per thread
+constexpr int RPT = 4;  // rows per thread per band (register window of RPT + 2 rows)
 
 __host__ __device__ constexpr int term_index(int i, int j) { return (i + j) * (i + j + 1) / 2 + j; }
 
@@ -45,11 +50,42 @@ __device__ __forceinline__ float poly(const float (&c)[15], float hx, float hy) 
   return acc;
 }
 
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+
+// The same polynomial for two pixels at once on the packed pipe; the final
+// Horner step is scalar so that it carries the [0,1] saturation for free.
+template <int DEG>
+__device__ __forceinline__ float2 poly2_sat(const float (&c)[15], float2 hx, float2 hy) {
+  float2 acc = bc(0.f);
+  float2 out = bc(0.f);
+#pragma unroll
+  for (int i = DEG; i >= 0; --i) {
+    float2 p = bc(c[term_index(i, DEG - i)]);
+#pragma unroll
+    for (int j = DEG - i - 1; j >= 0; --j) {
+      p = (j == DEG - i - 1) ? __ffma2_rn(hy, bc(c[term_index(i, DEG - i)]), bc(c[term_index(i, j)]))
+                             : __ffma2_rn(p, hy, bc(c[term_index(i, j)]));
+    }
+    if (i == DEG) {
+      acc = p;
+    } else if (i > 0) {
+      acc = __ffma2_rn(acc, hx, p);
+    } else {
+      out.x = __saturatef(__fmaf_rn(acc.x, hx.x, p.x));
+      out.y = __saturatef(__fmaf_rn(acc.y, hx.y, p.y));
+    }
+  }
+  return out;
+}
+
 __device__ __forceinline__ uint32_t q8(float x) {
   // clip(rint(255 x), 0, 255): x is saturated to [0,1] first, then the
   // 1.5*2^23 bias rounds the exact product half-to-even into the low byte.
   return __float_as_uint(__fmaf_rn(__saturatef(x), 255.0f, 12582912.0f));
 }
+
+// two already-saturated values -> their biased quantised bit patterns
+__device__ __forceinline__ float2 q8x2(float2 v) { return __ffma2_rn(v, bc(255.0f), bc(12582912.0f)); }
 
 template <int DEG>
 __device__ __forceinline__ void shade(const LutParams& L, float hx, float hy, float& r, float& g, float& b) {
@@ -58,29 +94,42 @@ __device__ __forceinline__ void shade(const LutParams& L, float hx, float hy, fl
   b = __saturatef(poly<DEG>(L.c[2], hx, hy));
 }
 
-struct Smem {
-  int band, stages, W;
+struct Layout {
+  int band, rpt, groups, stages;
   size_t in_stage_floats, out_stage_bytes;
   static constexpr size_t kBarBytes = 128;
-  __host__ __device__ size_t bytes(bool u8) const {
+  size_t bytes(bool u8) const {
     return kBarBytes + stages * in_stage_floats * sizeof(float) + (u8 ? 2 * out_stage_bytes : 0);
   }
 };
 
 template <int DEG, bool U8, bool F32>
-__global__ void __launch_bounds__(kThreads) rgb_bulk_kernel(const float* __restrict__ depth, int64_t n_images,
-                                                            int H, int W, int band, int stages,
-                                                            uint8_t* __restrict__ out_u8,
-                                                            float* __restrict__ out_f32, const LutParams L,
-                                                            int bulk_store) {
+__global__ void __launch_bounds__(kMaxThreads, 2) rgb_bulk_kernel(const float* __restrict__ depth, int64_t n_images,
+                                                               int H, int W, int stages,
+                                                               uint8_t* __restrict__ out_u8,
+                                                               float* __restrict__ out_f32, const LutParams L,
+                                                               int bulk_store) {
   extern __shared__ __align__(128) unsigned char smem[];
+  const int QW = W >> 2;
+  const int groups = blockDim.x / QW;  // host guarantees blockDim.x == QW * groups
+  const int band = groups * RPT;
   const int bands = (H + band - 1) / band;
   const int64_t units = n_images * bands;
   const size_t in_stage = (size_t)(band + 2) * W;
   const size_t out_stage = (size_t)band * W * 3;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-  float* in_buf = reinterpret_cast<float*>(smem + Smem::kBarBytes);
+  float* in_buf = reinterpret_cast<float*>(smem + Layout::kBarBytes);
   uint8_t* out_buf = reinterpret_cast<uint8_t*>(in_buf + stages * in_stage);
+
+  // per-thread constants: column quad, row group, border handling
+  const int xq = threadIdx.x % QW;
+  const int g = threadIdx.x / QW;
+  const int x0 = xq << 2;
+  const bool at_left = (x0 == 0), at_right = (x0 + 4 >= W);
+  const int left_off = at_left ? x0 : x0 - 1;      // at the border "left" reads c.x ...
+  const int right_off = at_right ? x0 + 3 : x0 + 4; // ... and "right" reads c.w
+  const float m0 = at_left ? 2.f : 1.f;             // np.gradient one-sided borders are not halved:
+  const float m3 = at_right ? 2.f : 1.f;            // h = 2*(f1-f0) in the doubled-gradient form
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
@@ -110,7 +159,6 @@ __global__ void __launch_bounds__(kThreads) rgb_bulk_kernel(const float* __restr
     }
   }
 
-  const int QW = W >> 2;
   int it = 0;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
     const int s = it % stages;
@@ -124,53 +172,75 @@ __global__ void __launch_bounds__(kThreads) rgb_bulk_kernel(const float* __restr
     mbar_wait_parity(&bars[s], parity);
 
     const float* tile = in_buf + (size_t)s * in_stage + W;  // tile row lr = image row r0 + lr
-    const int items = nrows * QW;
-    for (int q = threadIdx.x; q < items; q += kThreads) {
-      const int lr = q / QW;
-      const int x0 = (q - lr * QW) << 2;
-      const int r = r0 + lr;
-      const float* rowc = tile + (size_t)lr * W;
-      const float4 c = *reinterpret_cast<const float4*>(rowc + x0);
-      float4 hy;
-      if (r > 0 && r < H - 1) {
-        const float4 up = *reinterpret_cast<const float4*>(rowc - W + x0);
-        const float4 dn = *reinterpret_cast<const float4*>(rowc + W + x0);
-        hy = make_float4(dn.x - up.x, dn.y - up.y, dn.z - up.z, dn.w - up.w);
-      } else if (r == 0) {
-        const float4 dn = *reinterpret_cast<const float4*>(rowc + W + x0);
-        hy = make_float4(2.f * (dn.x - c.x), 2.f * (dn.y - c.y), 2.f * (dn.z - c.z), 2.f * (dn.w - c.w));
-      } else {
-        const float4 up = *reinterpret_cast<const float4*>(rowc - W + x0);
-        hy = make_float4(2.f * (c.x - up.x), 2.f * (c.y - up.y), 2.f * (c.z - up.z), 2.f * (c.w - up.w));
-      }
-      float4 hx;
-      hx.x = (x0 > 0) ? c.y - rowc[x0 - 1] : 2.f * (c.y - c.x);
-      hx.y = c.z - c.x;
-      hx.z = c.w - c.y;
-      hx.w = (x0 + 4 < W) ? rowc[x0 + 4] - c.z : 2.f * (c.w - c.z);
-
-      float v[12];
-      shade<DEG>(L, hx.x, hy.x, v[0], v[1], v[2]);
-      shade<DEG>(L, hx.y, hy.y, v[3], v[4], v[5]);
-      shade<DEG>(L, hx.z, hy.z, v[6], v[7], v[8]);
-      shade<DEG>(L, hx.w, hy.w, v[9], v[10], v[11]);
-      if (U8) {
-        uint32_t b[12];
+    const int lr0 = g * RPT;
+    if (lr0 < nrows) {
+      // register window: win[k] = image row r0 + lr0 - 1 + k; a missing row
+      // (above the image / below it) repeats its neighbour, which together
+      // with the x2 below gives np.gradient's one-sided border rows
+      const float* col = tile + (size_t)lr0 * W + x0;
+      float4 win[RPT + 2];
+      win[1] = *reinterpret_cast<const float4*>(col);
+      win[0] = (r0 + lr0 > 0) ? *reinterpret_cast<const float4*>(col - W) : win[1];
 #pragma unroll
-        for (int k = 0; k < 12; ++k) b[k] = q8(v[k]);
-        uint32_t w0 = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
-        uint32_t w1 = __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
-        uint32_t w2 = __byte_perm(__byte_perm(b[8], b[9], 0x0040), __byte_perm(b[10], b[11], 0x0040), 0x5410);
-        uint32_t* o = reinterpret_cast<uint32_t*>(ob + ((size_t)lr * W + x0) * 3);
-        o[0] = w0;
-        o[1] = w1;
-        o[2] = w2;
+      for (int k = 1; k <= RPT; ++k)
+        win[k + 1] = (r0 + lr0 + k <= H - 1) ? *reinterpret_cast<const float4*>(col + (size_t)k * W) : win[k];
+      float hl[RPT], hr[RPT];
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const float* row = tile + (size_t)(lr0 + j) * W;
+        hl[j] = row[left_off];
+        hr[j] = row[right_off];
       }
-      if (F32) {
-        float4* o = reinterpret_cast<float4*>(out_f32 + (((size_t)img * H + r) * W + x0) * 3);
-        o[0] = make_float4(v[0], v[1], v[2], v[3]);
-        o[1] = make_float4(v[4], v[5], v[6], v[7]);
-        o[2] = make_float4(v[8], v[9], v[10], v[11]);
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int lr = lr0 + j;
+        if (lr >= nrows) break;
+        const int r = r0 + lr;
+        const float4 up = win[j], c = win[j + 1], dn = win[j + 2];
+        const float left = hl[j], right = hr[j];
+        // doubled gradients h = 2g (coefficients carry the 2^-(i+j))
+        float2 hy01 = __fadd2_rn(make_float2(dn.x, dn.y), make_float2(-up.x, -up.y));
+        float2 hy23 = __fadd2_rn(make_float2(dn.z, dn.w), make_float2(-up.z, -up.w));
+        if (r == 0 || r == H - 1) {  // one-sided rows: 2*(f1-f0)
+          hy01 = __fadd2_rn(hy01, hy01);
+          hy23 = __fadd2_rn(hy23, hy23);
+        }
+        const float2 hx01 = make_float2((c.y - left) * m0, c.z - c.x);
+        const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
+        const float2 r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
+        const float2 g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
+        const float2 b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
+        const float2 r23 = poly2_sat<DEG>(L.c[0], hx23, hy23);
+        const float2 g23 = poly2_sat<DEG>(L.c[1], hx23, hy23);
+        const float2 b23 = poly2_sat<DEG>(L.c[2], hx23, hy23);
+        if (U8) {
+          // pixel order p0..p3, channel-interleaved: (r0 g0 b0 r1)(g1 b1 r2 g2)(b2 r3 g3 b3)
+          const float2 qa = q8x2(make_float2(r01.x, g01.x));
+          const float2 qb = q8x2(make_float2(b01.x, r01.y));
+          const float2 qc = q8x2(make_float2(g01.y, b01.y));
+          const float2 qd = q8x2(make_float2(r23.x, g23.x));
+          const float2 qe = q8x2(make_float2(b23.x, r23.y));
+          const float2 qf = q8x2(make_float2(g23.y, b23.y));
+          const uint32_t w0 = __byte_perm(__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040),
+                                          __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040),
+                                          0x5410);
+          const uint32_t w1 = __byte_perm(__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040),
+                                          __byte_perm(__float_as_uint(qd.x), __float_as_uint(qd.y), 0x0040),
+                                          0x5410);
+          const uint32_t w2 = __byte_perm(__byte_perm(__float_as_uint(qe.x), __float_as_uint(qe.y), 0x0040),
+                                          __byte_perm(__float_as_uint(qf.x), __float_as_uint(qf.y), 0x0040),
+                                          0x5410);
+          uint32_t* o = reinterpret_cast<uint32_t*>(ob + ((size_t)lr * W + x0) * 3);
+          o[0] = w0;
+          o[1] = w1;
+          o[2] = w2;
+        }
+        if (F32) {
+          float4* o = reinterpret_cast<float4*>(out_f32 + (((size_t)img * H + r) * W + x0) * 3);
+          o[0] = make_float4(r01.x, g01.x, b01.x, r01.y);
+          o[1] = make_float4(g01.y, b01.y, r23.x, g23.x);
+          o[2] = make_float4(b23.x, r23.y, g23.y, b23.y);
+        }
       }
     }
     if (U8) fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
@@ -186,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) rgb_bulk_kernel(const float* __restr
       } else {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(ob);
         uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-        for (uint32_t k = threadIdx.x; k < bytes / 4; k += kThreads) d32[k] = src[k];
+        for (uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x) d32[k] = src[k];
       }
     }
     if (threadIdx.x == 0) {
@@ -200,9 +270,9 @@ __global__ void __launch_bounds__(kThreads) rgb_bulk_kernel(const float* __restr
 // Generic path (any W >= 2, any alignment): one thread per pixel, neighbours
 // straight from global memory through L1.
 template <int DEG>
-__global__ void __launch_bounds__(kThreads) rgb_scalar_kernel(const float* __restrict__ depth, int64_t n_images,
-                                                              int H, int W, uint8_t* __restrict__ out_u8,
-                                                              float* __restrict__ out_f32, const LutParams L) {
+__global__ void __launch_bounds__(256) rgb_scalar_kernel(const float* __restrict__ depth, int64_t n_images, int H,
+                                                         int W, uint8_t* __restrict__ out_u8,
+                                                         float* __restrict__ out_f32, const LutParams L) {
   const int64_t total = n_images * (int64_t)H * W;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += stride) {
@@ -241,15 +311,30 @@ int env_int(const char* name, int dflt) {
   return v > 0 ? v : dflt;
 }
 
+// Row groups / rows per thread / ring depth.  Defaults keep ~100 KB of shared
+// memory per CTA (two CTAs per SM) with >= 2 bands per CTA in flight.
+Layout choose_layout(int H, int W, bool u8) {
+  const int QW = W / 4;
+  Layout lay;
+  lay.rpt = RPT;
+  int groups = env_int("TACSL_RGB_GROUPS", std::max(1, std::min(kMaxThreads / QW, 320 / QW > 0 ? 320 / QW : 1)));
+  groups = std::max(1, std::min(groups, kMaxThreads / QW));
+  // no point in more groups than the image has rows
+  while (groups > 1 && (groups - 1) * lay.rpt >= H) --groups;
+  lay.groups = groups;
+  lay.band = groups * lay.rpt;
+  lay.stages = env_int("TACSL_RGB_STAGES", 3);
+  lay.in_stage_floats = (size_t)(lay.band + 2) * W;
+  lay.out_stage_bytes = (size_t)lay.band * W * 3;
+  (void)u8;
+  return lay;
+}
+
 template <int DEG, bool U8, bool F32>
 int launch_bulk(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32, const LutParams& L,
                 cudaStream_t stream) {
-  // band: 16 rows (8 at W > 512) keeps a 3-stage input ring + 2 output tiles
-  // near 100 KB, i.e. two resident CTAs per SM with ~6 bands in flight.
-  int band = env_int("TACSL_RGB_BAND", W > 512 ? 8 : 16);
-  int stages = env_int("TACSL_RGB_STAGES", 3);
-  band = std::min(band, H);
-  Smem lay{band, stages, W, (size_t)(band + 2) * W, (size_t)band * W * 3};
+  Layout lay = choose_layout(H, W, U8);
+  const int threads = (W / 4) * lay.groups;
   size_t smem = lay.bytes(U8);
   auto kern = rgb_bulk_kernel<DEG, U8, F32>;
   static std::mutex mu;
@@ -263,21 +348,22 @@ int launch_bulk(const float* depth, int64_t n, int H, int W, uint8_t* u8, float*
     }
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-  if (per_sm <= 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: image too wide for the shared-memory ring");
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm <= 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: band ring does not fit in shared memory");
   per_sm = std::min(per_sm, env_int("TACSL_RGB_CTAS_PER_SM", per_sm));
-  const int bands = (H + band - 1) / band;
+  const int bands = (H + lay.band - 1) / lay.band;
   const int64_t units = n * bands;
   int64_t grid = std::min<int64_t>(units, (int64_t)sm_count(current_device()) * per_sm);
   const int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
-  kern<<<(unsigned)grid, kThreads, smem, stream>>>(depth, n, H, W, band, stages, u8, f32, L, bulk_store);
+  kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.stages, u8, f32, L, bulk_store);
   return check_launch("rgb_bulk_kernel");
 }
 
 template <int DEG>
 int dispatch(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32, const LutParams& L,
              cudaStream_t stream) {
-  const bool aligned = (W % 4 == 0) && ((reinterpret_cast<uintptr_t>(depth) & 15) == 0) &&
+  const bool aligned = (W % 4 == 0) && (W / 4 <= kMaxThreads) &&
+                       ((reinterpret_cast<uintptr_t>(depth) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(f32) & 15) == 0) && ((reinterpret_cast<uintptr_t>(u8) & 3) == 0);
   if (aligned && !std::getenv("TACSL_RGB_FORCE_SCALAR")) {
     if (u8 && f32) return launch_bulk<DEG, true, true>(depth, n, H, W, u8, f32, L, stream);
@@ -285,8 +371,8 @@ int dispatch(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f3
     return launch_bulk<DEG, false, true>(depth, n, H, W, u8, f32, L, stream);
   }
   const int64_t total = n * (int64_t)H * W;
-  int64_t blocks = std::min<int64_t>((total + kThreads - 1) / kThreads, (int64_t)sm_count(current_device()) * 16);
-  rgb_scalar_kernel<DEG><<<(unsigned)blocks, kThreads, 0, stream>>>(depth, n, H, W, u8, f32, L);
+  int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(current_device()) * 16);
+  rgb_scalar_kernel<DEG><<<(unsigned)blocks, 256, 0, stream>>>(depth, n, H, W, u8, f32, L);
   return check_launch("rgb_scalar_kernel");
 }
 

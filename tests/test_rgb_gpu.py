@@ -127,13 +127,13 @@ def test_rgb_scalar_path_equals_bulk_path(monkeypatch):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("band,stages", [(1, 2), (7, 3), (16, 4), (60, 1)])
-def test_rgb_pipeline_shapes(monkeypatch, band, stages):
+@pytest.mark.parametrize("groups,stages", [(1, 2), (2, 3), (4, 4), (6, 1), (5, 2), (13, 2)])
+def test_rgb_pipeline_shapes(monkeypatch, groups, stages):
     size = (320, 240)
     _, cam, bg, lut, _ = synthetic.sensor_setup(size)
     d = torch.from_numpy(synthetic.depth_batch(cam, bg, 5, config_id=9)).cuda()
     ref = depth_to_rgb(d, lut, out_dtype=np.uint8)
-    monkeypatch.setenv("TACSL_RGB_BAND", str(band))
+    monkeypatch.setenv("TACSL_RGB_GROUPS", str(groups))
     monkeypatch.setenv("TACSL_RGB_STAGES", str(stages))
     assert torch.equal(depth_to_rgb(d, lut, out_dtype=np.uint8), ref)
 

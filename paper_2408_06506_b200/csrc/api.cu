@@ -110,17 +110,15 @@ int tacsl_sdf_create(int device, const double* values, const double* gradients, 
   if (!tacsl_device_supported(device))
     return set_error(TACSL_ERR_NO_DEVICE, "sdf_create: device is not an sm_100 (B200) GPU");
   const size_t n = (size_t)dims[0] * dims[1] * dims[2];
-  std::vector<double2> host(2 * n);
-  for (size_t i = 0; i < n; ++i) {
-    host[2 * i] = make_double2(values[i], gradients[3 * i + 0]);
-    host[2 * i + 1] = make_double2(gradients[3 * i + 1], gradients[3 * i + 2]);
-  }
+  std::vector<double4> host(n);
+  for (size_t i = 0; i < n; ++i)
+    host[i] = make_double4(values[i], gradients[3 * i + 0], gradients[3 * i + 1], gradients[3 * i + 2]);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  double2* dptr = nullptr;
-  cudaError_t e = cudaMalloc(&dptr, 2 * n * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMemcpy(dptr, host.data(), 2 * n * sizeof(double2), cudaMemcpyHostToDevice);
+  double4* dptr = nullptr;
+  cudaError_t e = cudaMalloc(&dptr, n * sizeof(double4));
+  if (e == cudaSuccess) e = cudaMemcpy(dptr, host.data(), n * sizeof(double4), cudaMemcpyHostToDevice);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     if (dptr) cudaFree(dptr);

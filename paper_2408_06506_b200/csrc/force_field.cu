@@ -65,10 +65,92 @@ __device__ __forceinline__ V3 quat_rotate(double w, V3 qv, V3 v) {
 __device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 
 struct Grid {
-  const double2* __restrict__ cells;  // 2 per cell: (d, gx), (gy, gz)
+  const double4* __restrict__ cells;  // {d, gx, gy, gz} per cell, z fastest
   int nx, ny, nz;
   double ox, oy, oz, spacing;
 };
+
+// 256-bit read-only load (LDG.E.ENL2.256 on sm_100): one trilinear corner
+__device__ __forceinline__ double4 ldg256(const double4* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+// Cell location and trilinear weights of a query point (sdf.py:280-290)
+struct Cell {
+  size_t base;
+  double wx, wy, wz, ux, uy, uz;
+  bool valid;
+};
+
+__device__ __forceinline__ Cell locate(const Grid& g, V3 p) {
+  const double rx = __ddiv_rn(sub_rn(p.x, g.ox), g.spacing);
+  const double ry = __ddiv_rn(sub_rn(p.y, g.oy), g.spacing);
+  const double rz = __ddiv_rn(sub_rn(p.z, g.oz), g.spacing);
+  const double mx = (double)(g.nx - 1), my = (double)(g.ny - 1), mz = (double)(g.nz - 1);
+  Cell c;
+  c.valid = (rx >= 0.0) & (rx <= mx) & (ry >= 0.0) & (ry <= my) & (rz >= 0.0) & (rz <= mz);
+  // clip(rel, 0, dims - 1 - 1e-9); i0 = min(int(rel_c), dims - 2); f = rel_c - i0
+  const double cx = fmin(fmax(rx, 0.0), sub_rn(mx, 1e-9));
+  const double cy = fmin(fmax(ry, 0.0), sub_rn(my, 1e-9));
+  const double cz = fmin(fmax(rz, 0.0), sub_rn(mz, 1e-9));
+  const int ix = min((int)cx, g.nx - 2), iy = min((int)cy, g.ny - 2), iz = min((int)cz, g.nz - 2);
+  c.wx = sub_rn(cx, (double)ix);
+  c.wy = sub_rn(cy, (double)iy);
+  c.wz = sub_rn(cz, (double)iz);
+  c.ux = sub_rn(1.0, c.wx);
+  c.uy = sub_rn(1.0, c.wy);
+  c.uz = sub_rn(1.0, c.wz);
+  c.base = ((size_t)ix * g.ny + iy) * g.nz + iz;
+  return c;
+}
+
+// corner k = 4*dx + 2*dy + dz
+__device__ __forceinline__ size_t corner(const Grid& g, const Cell& c, int k) {
+  return c.base + (size_t)((k >> 2) & 1) * g.ny * g.nz + (size_t)((k >> 1) & 1) * g.nz + (k & 1);
+}
+
+// Trilinear distance, x then y then z lerps with every product and sum
+// rounded separately, as numpy evaluates sdf.py:305-311 -- bit-exact.
+__device__ __forceinline__ double interp_d(const Grid& g, const Cell& c) {
+  double v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __ldg(&g.cells[corner(g, c, k)].x);
+  const double d00 = add_rn(mul_rn(v[0], c.ux), mul_rn(v[4], c.wx));
+  const double d10 = add_rn(mul_rn(v[2], c.ux), mul_rn(v[6], c.wx));
+  const double d01 = add_rn(mul_rn(v[1], c.ux), mul_rn(v[5], c.wx));
+  const double d11 = add_rn(mul_rn(v[3], c.ux), mul_rn(v[7], c.wx));
+  const double d0 = add_rn(mul_rn(d00, c.uy), mul_rn(d10, c.wy));
+  const double d1 = add_rn(mul_rn(d01, c.uy), mul_rn(d11, c.wy));
+  return add_rn(mul_rn(d0, c.uz), mul_rn(d1, c.wz));
+}
+
+// Trilinear gradient, renormalised: n = g / max(|g|, 1e-12) (sdf.py:314-316)
+__device__ __forceinline__ V3 interp_n(const Grid& g, const Cell& c) {
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  double ax[2], ay[2], az[2];
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    double bx[2], by[2], bz[2];
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const double4 lo = ldg256(g.cells + corner(g, c, 2 * dy + dz));
+      const double4 hi = ldg256(g.cells + corner(g, c, 4 + 2 * dy + dz));
+      bx[dy] = lo.y * c.ux + hi.y * c.wx;
+      by[dy] = lo.z * c.ux + hi.z * c.wx;
+      bz[dy] = lo.w * c.ux + hi.w * c.wx;
+    }
+    ax[dz] = bx[0] * c.uy + bx[1] * c.wy;
+    ay[dz] = by[0] * c.uy + by[1] * c.wy;
+    az[dz] = bz[0] * c.uy + bz[1] * c.wy;
+  }
+  gx = ax[0] * c.uz + ax[1] * c.wz;
+  gy = ay[0] * c.uz + ay[1] * c.wz;
+  gz = az[0] * c.uz + az[1] * c.wz;
+  const double inv = rsqrt(fmax(gx * gx + gy * gy + gz * gz, 1e-24));
+  return v3(gx * inv, gy * inv, gz * inv);
+}
 
 struct Query {
   double d;  // +inf when outside
@@ -76,60 +158,14 @@ struct Query {
   bool valid;
 };
 
-// geometry/sdf.py:277-318
+// geometry/sdf.py:271-321
 __device__ __forceinline__ Query query(const Grid& g, V3 p) {
-  const double rx = __ddiv_rn(sub_rn(p.x, g.ox), g.spacing);
-  const double ry = __ddiv_rn(sub_rn(p.y, g.oy), g.spacing);
-  const double rz = __ddiv_rn(sub_rn(p.z, g.oz), g.spacing);
-  const double mx = (double)(g.nx - 1), my = (double)(g.ny - 1), mz = (double)(g.nz - 1);
+  const Cell c = locate(g, p);
   Query q;
-  q.valid = (rx >= 0.0) & (rx <= mx) & (ry >= 0.0) & (ry <= my) & (rz >= 0.0) & (rz <= mz);
-  // clip(rel, 0, dims - 1 - 1e-9); i0 = min(int(rel_c), dims - 2); f = rel_c - i0
-  const double cx = fmin(fmax(rx, 0.0), sub_rn(mx, 1e-9));
-  const double cy = fmin(fmax(ry, 0.0), sub_rn(my, 1e-9));
-  const double cz = fmin(fmax(rz, 0.0), sub_rn(mz, 1e-9));
-  const int ix = min((int)cx, g.nx - 2), iy = min((int)cy, g.ny - 2), iz = min((int)cz, g.nz - 2);
-  const double wx = sub_rn(cx, (double)ix), wy = sub_rn(cy, (double)iy), wz = sub_rn(cz, (double)iz);
-  const double ux = sub_rn(1.0, wx), uy = sub_rn(1.0, wy), uz = sub_rn(1.0, wz);
-
-  const size_t sz = (size_t)g.nz, sy = (size_t)g.ny * g.nz;
-  const size_t base = (size_t)ix * sy + (size_t)iy * sz + iz;
-  // corner (a,b,c) -> two 16B loads: (d, gx) and (gy, gz)
-  double2 A[8], B[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const size_t cell = base + ((k >> 2) & 1) * sy + ((k >> 1) & 1) * sz + (k & 1);
-    A[k] = __ldg(g.cells + 2 * cell);
-    B[k] = __ldg(g.cells + 2 * cell + 1);
-  }
-  // k = 4*dx + 2*dy + dz
-  // distance: x, then y, then z lerps, products and sums rounded separately (sdf.py:305-311)
-  {
-    const double d00 = add_rn(mul_rn(A[0].x, ux), mul_rn(A[4].x, wx));
-    const double d10 = add_rn(mul_rn(A[2].x, ux), mul_rn(A[6].x, wx));
-    const double d01 = add_rn(mul_rn(A[1].x, ux), mul_rn(A[5].x, wx));
-    const double d11 = add_rn(mul_rn(A[3].x, ux), mul_rn(A[7].x, wx));
-    const double d0 = add_rn(mul_rn(d00, uy), mul_rn(d10, wy));
-    const double d1 = add_rn(mul_rn(d01, uy), mul_rn(d11, wy));
-    q.d = add_rn(mul_rn(d0, uz), mul_rn(d1, wz));
-  }
-  // gradient: same lerp tree, contracted
-  auto lerp = [&](double a000, double a100, double a010, double a110, double a001, double a101, double a011,
-                  double a111) {
-    const double a00 = a000 * ux + a100 * wx;
-    const double a10 = a010 * ux + a110 * wx;
-    const double a01 = a001 * ux + a101 * wx;
-    const double a11 = a011 * ux + a111 * wx;
-    const double a0 = a00 * uy + a10 * wy;
-    const double a1 = a01 * uy + a11 * wy;
-    return a0 * uz + a1 * wz;
-  };
-  const double gx = lerp(A[0].y, A[4].y, A[2].y, A[6].y, A[1].y, A[5].y, A[3].y, A[7].y);
-  const double gy = lerp(B[0].x, B[4].x, B[2].x, B[6].x, B[1].x, B[5].x, B[3].x, B[7].x);
-  const double gz = lerp(B[0].y, B[4].y, B[2].y, B[6].y, B[1].y, B[5].y, B[3].y, B[7].y);
-  const double inv = 1.0 / fmax(sqrt(gx * gx + gy * gy + gz * gz), 1e-12);
-  if (q.valid) {
-    q.n = v3(gx * inv, gy * inv, gz * inv);
+  q.valid = c.valid;
+  if (c.valid) {
+    q.d = interp_d(g, c);
+    q.n = interp_n(g, c);
   } else {
     q.d = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     q.n = v3(0.0, 0.0, 0.0);
@@ -148,10 +184,12 @@ __device__ __forceinline__ void penalty(const Penalty& P, double d, double d_dot
   double coeff = contact ? (-P.k_n + P.k_d * d_dot) * d : 0.0;
   coeff = fmax(coeff, 0.0);
   fn = v3(coeff * n.x, coeff * n.y, coeff * n.z);
-  const double speed = sqrt(vt.x * vt.x + vt.y * vt.y + vt.z * vt.z);
+  const double ss = vt.x * vt.x + vt.y * vt.y + vt.z * vt.z;
+  const double inv = rsqrt(ss);
+  const double speed = ss > 0.0 ? ss * inv : 0.0;
   const bool slipping = contact && (speed > 1e-9);  // SLIP_VELOCITY_EPS, field.py:25
   const double mag = fmin(P.k_t * speed, P.mu * coeff);
-  const double scale = slipping ? mag / speed : 0.0;
+  const double scale = slipping ? mag * inv : 0.0;
   ft = v3(-scale * vt.x, -scale * vt.y, -scale * vt.z);
 }
 
@@ -179,7 +217,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 template <typename OutT>
-__global__ void __launch_bounds__(256) force_field_kernel(
+__global__ void __launch_bounds__(128, 4) force_field_kernel(
     const Grid grid, const double* __restrict__ taxels, int n_taxels, const double* __restrict__ obj_state,
     int64_t obj_stride, const double* __restrict__ sen_state, int64_t sen_stride, int n_sensors, const Penalty P,
     OutT* __restrict__ f_n_out, OutT* __restrict__ f_t_out, double* __restrict__ wrench, double* __restrict__ kin,
@@ -191,6 +229,7 @@ __global__ void __launch_bounds__(256) force_field_kernel(
   const State S = load_state(sen_state + e * sen_stride + (int64_t)s * 13);
   const V3 oq_inv = v3(-O.qv.x, -O.qv.y, -O.qv.z);
   const V3 sq_inv = v3(-S.qv.x, -S.qv.y, -S.qv.z);
+  const bool want_kin = kin != nullptr;
 
   double acc[6] = {0, 0, 0, 0, 0, 0};
   const int64_t out_base = frame * (int64_t)n_taxels;
@@ -201,21 +240,52 @@ __global__ void __launch_bounds__(256) force_field_kernel(
     pw = v3(add_rn(pw.x, S.pos.x), add_rn(pw.y, S.pos.y), add_rn(pw.z, S.pos.z));
     const V3 ro = v3(sub_rn(pw.x, O.pos.x), sub_rn(pw.y, O.pos.y), sub_rn(pw.z, O.pos.z));
     const V3 po = quat_rotate_rn(O.qw, oq_inv, ro);
-    const Query q = query(grid, po);
-    // ---- kinematics (field.py:109-115) ----
-    const V3 nw = quat_rotate(O.qw, O.qv, q.n);
-    const V3 rs = v3(pw.x - S.pos.x, pw.y - S.pos.y, pw.z - S.pos.z);
-    const V3 cs = cross(S.w, rs), co = cross(O.w, ro);
-    const V3 xd = v3((S.v.x + cs.x) - (O.v.x + co.x), (S.v.y + cs.y) - (O.v.y + co.y),
-                     (S.v.z + cs.z) - (O.v.z + co.z));
-    const double d_dot = dot(nw, xd);
-    const V3 vt = v3(xd.x - d_dot * nw.x, xd.y - d_dot * nw.y, xd.z - d_dot * nw.z);
-    V3 fnw, ftw;
-    bool contact;
-    penalty(P, q.d, d_dot, nw, vt, fnw, ftw, contact);
-    // ---- back to the sensor frame (field.py:118-119) ----
-    const V3 fn = quat_rotate(S.qw, sq_inv, fnw);
-    const V3 ft = quat_rotate(S.qw, sq_inv, ftw);
+    const Cell cell = locate(grid, po);
+    const double d = cell.valid ? interp_d(grid, cell) : __longlong_as_double(0x7ff0000000000000LL);
+    const bool contact = d < 0.0;  // field.py:64
+    V3 fn = v3(0.0, 0.0, 0.0), ft = v3(0.0, 0.0, 0.0);
+    // Out of contact both forces are exactly zero (field.py:65-75), so the
+    // normal, the velocities and the penalty law run only for contact
+    // taxels -- unless the caller asked for the kinematics of every taxel.
+    if (contact || want_kin) {
+      const V3 n = cell.valid ? interp_n(grid, cell) : v3(0.0, 0.0, 0.0);
+      // ---- kinematics (field.py:109-115) ----
+      const V3 nw = quat_rotate(O.qw, O.qv, n);
+      const V3 rs = v3(pw.x - S.pos.x, pw.y - S.pos.y, pw.z - S.pos.z);
+      const V3 cs = cross(S.w, rs), co = cross(O.w, ro);
+      const V3 xd = v3((S.v.x + cs.x) - (O.v.x + co.x), (S.v.y + cs.y) - (O.v.y + co.y),
+                       (S.v.z + cs.z) - (O.v.z + co.z));
+      const double d_dot = dot(nw, xd);
+      const V3 vt = v3(xd.x - d_dot * nw.x, xd.y - d_dot * nw.y, xd.z - d_dot * nw.z);
+      if (contact) {
+        V3 fnw, ftw;
+        bool c2;
+        penalty(P, d, d_dot, nw, vt, fnw, ftw, c2);
+        // ---- back to the sensor frame (field.py:118-119) ----
+        fn = quat_rotate(S.qw, sq_inv, fnw);
+        ft = quat_rotate(S.qw, sq_inv, ftw);
+        // ---- net wrench (field.py:132-141) ----
+        const V3 f = v3(fn.x + ft.x, fn.y + ft.y, fn.z + ft.z);
+        const V3 tq = cross(p, f);
+        acc[0] += f.x;
+        acc[1] += f.y;
+        acc[2] += f.z;
+        acc[3] += tq.x;
+        acc[4] += tq.y;
+        acc[5] += tq.z;
+      }
+      if (want_kin) {
+        double* k = kin + (out_base + i) * 8;
+        k[0] = d;
+        k[1] = d_dot;
+        k[2] = vt.x;
+        k[3] = vt.y;
+        k[4] = vt.z;
+        k[5] = nw.x;
+        k[6] = nw.y;
+        k[7] = nw.z;
+      }
+    }
     const int64_t o = (out_base + i) * 3;
     f_n_out[o + 0] = (OutT)fn.x;
     f_n_out[o + 1] = (OutT)fn.y;
@@ -223,27 +293,7 @@ __global__ void __launch_bounds__(256) force_field_kernel(
     f_t_out[o + 0] = (OutT)ft.x;
     f_t_out[o + 1] = (OutT)ft.y;
     f_t_out[o + 2] = (OutT)ft.z;
-    if (kin) {
-      double* k = kin + (out_base + i) * 8;
-      k[0] = q.d;
-      k[1] = d_dot;
-      k[2] = vt.x;
-      k[3] = vt.y;
-      k[4] = vt.z;
-      k[5] = nw.x;
-      k[6] = nw.y;
-      k[7] = nw.z;
-    }
     if (contact_out) contact_out[out_base + i] = contact ? 1 : 0;
-    // ---- net wrench (field.py:132-141) ----
-    const V3 f = v3(fn.x + ft.x, fn.y + ft.y, fn.z + ft.z);
-    const V3 tq = cross(p, f);
-    acc[0] += f.x;
-    acc[1] += f.y;
-    acc[2] += f.z;
-    acc[3] += tq.x;
-    acc[4] += tq.y;
-    acc[5] += tq.z;
   }
   if (wrench) {
     __shared__ double part[8][6];
@@ -402,7 +452,7 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
   if (!taxels || !object_state || !sensor_state || !f_n || !f_t)
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "force_field: null pointer");
   const int n_taxels = rows * cols;
-  const int threads = n_taxels <= 1024 ? 128 : 256;
+  const int threads = 128;
   Penalty P{params.k_n, params.k_d, params.k_t, params.mu};
   cudaStream_t s = (cudaStream_t)stream;
   if (out_fp64) {

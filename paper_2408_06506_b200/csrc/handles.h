@@ -25,7 +25,7 @@ struct tacsl_lut_s {
 
 struct tacsl_sdf_s {
   int device;
-  double2* grid;  // (nx, ny, nz) x {(d, gx), (gy, gz)}, z fastest
+  double4* grid;  // (nx, ny, nz) {d, gx, gy, gz}, z fastest, 32 B per cell
   int dims[3];
   double origin[3];
   double spacing;

@@ -7,7 +7,7 @@
 //
 // Layout: depth (N, H, W) fp32, rgb (N, H, W, 3) HWC, u8 and/or fp32.
 //
-// Fast path (W % 4 == 0, W <= 1536, 16B-aligned pointers): persistent CTAs
+// Fast path (W % 4 == 0, W <= 1280, 16B-aligned pointers): persistent CTAs
 // walk work units = (image, band of B rows).  Thread 0 streams each band
 // plus its two halo rows global->shared with ONE bulk-async copy
 // (cp.async.bulk, the 1-D TMA engine) into a STAGES-deep ring completed on
@@ -30,8 +30,10 @@
 namespace tacsl {
 namespace {
 
-constexpr int kMaxThreads = 384;  // with 2 CTAs/SM: <= 85 registers per thread
-constexpr int RPT = 4;  // rows per thread per band (register window of RPT + 2 rows)
+constexpr int kMaxThreads = 320;  // consumer threads; + 2 producer warps = 384, 2 CTAs/SM: <= 85 registers
+constexpr int kMaxStages = 6;
+constexpr size_t kSmemPerSm = 227 * 1024;  // opt-in dynamic shared memory per CTA on sm_100
+constexpr int kDefaultRpt = 8;  // rows per thread per band (rolling 3-row register window)
 
 __host__ __device__ constexpr int term_index(int i, int j) { return (i + j) * (i + j + 1) / 2 + j; }
 
@@ -103,101 +105,150 @@ struct Layout {
   }
 };
 
-template <int DEG, bool U8, bool F32>
-__global__ void __launch_bounds__(kMaxThreads, 2) rgb_bulk_kernel(const float* __restrict__ depth, int64_t n_images,
-                                                               int H, int W, int stages,
-                                                               uint8_t* __restrict__ out_u8,
-                                                               float* __restrict__ out_f32, const LutParams L,
-                                                               int bulk_store) {
+// Warp roles.  Consumer warps (the first ceil(QW*groups/32) warps) shade;
+// the next warp streams bands in, the last one streams RGB out.  Stages and
+// output tiles change hands through mbarriers only -- no CTA-wide barrier in
+// the steady state, so consumer warps drift freely across bands.
+//   full[s]  : TMA transaction barrier, band landed in stage s
+//   empty[s] : every consumer warp has its rows of stage s in registers
+//   ready[b] : every consumer warp wrote its part of output tile b
+//   ofree[b] : the bulk store of tile b has finished reading it
+template <int DEG, int RPT, bool U8, bool F32>
+__global__ void __launch_bounds__(kMaxThreads + 64, 1) rgb_bulk_kernel(const float* __restrict__ depth,
+                                                                    int64_t n_images, int H, int W, int groups,
+                                                                    int stages, uint8_t* __restrict__ out_u8,
+                                                                    float* __restrict__ out_f32, const LutParams L,
+                                                                    int bulk_store) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int QW = W >> 2;
-  const int groups = blockDim.x / QW;  // host guarantees blockDim.x == QW * groups
+  const int n_cons = QW * groups;
+  const int cons_warps = (n_cons + 31) >> 5;  // host: blockDim.x == 32 * cons_warps + 64
   const int band = groups * RPT;
   const int bands = (H + band - 1) / band;
   const int64_t units = n_images * bands;
   const size_t in_stage = (size_t)(band + 2) * W;
   const size_t out_stage = (size_t)band * W * 3;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* ready = empty + kMaxStages;
+  uint64_t* ofree = ready + 2;
   float* in_buf = reinterpret_cast<float*>(smem + Layout::kBarBytes);
   uint8_t* out_buf = reinterpret_cast<uint8_t*>(in_buf + stages * in_stage);
-
-  // per-thread constants: column quad, row group, border handling
-  const int xq = threadIdx.x % QW;
-  const int g = threadIdx.x / QW;
-  const int x0 = xq << 2;
-  const bool at_left = (x0 == 0), at_right = (x0 + 4 >= W);
-  const int left_off = at_left ? x0 : x0 - 1;      // at the border "left" reads c.x ...
-  const int right_off = at_right ? x0 + 3 : x0 + 4; // ... and "right" reads c.w
-  const float m0 = at_left ? 2.f : 1.f;             // np.gradient one-sided borders are not halved:
-  const float m3 = at_right ? 2.f : 1.f;            // h = 2*(f1-f0) in the doubled-gradient form
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], cons_warps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ready[b], cons_warps);
+      mbar_init(&ofree[b], 1);
+    }
     fence_mbar_init();
     fence_proxy_async_smem();
   }
   __syncthreads();
 
-  // Stage s row 0 holds image row r0-1 (absent for the top band); rows that
-  // do not exist are never read.
-  auto issue = [&](int64_t u, int s) {
-    const int64_t img = u / bands;
-    const int r0 = (int)(u - img * bands) * band;
-    const int rs = max(r0 - 1, 0);
-    const int re = min(r0 + band, H - 1);
-    const uint32_t bytes = (uint32_t)(re - rs + 1) * (uint32_t)W * 4u;
-    float* dst = in_buf + (size_t)s * in_stage + (size_t)(rs - (r0 - 1)) * W;
-    const float* src = depth + ((size_t)img * H + rs) * (size_t)W;
-    mbar_arrive_expect_tx(&bars[s], bytes);
-    bulk_g2s(dst, src, bytes, &bars[s]);
-  };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      const int64_t u = (int64_t)blockIdx.x + (int64_t)s * gridDim.x;
-      if (u < units) issue(u, s);
+  if (warp == cons_warps) {
+    // ---------------------------------------------------------- loader ---
+    if (lane == 0) {
+      int k = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % stages;
+        if (k >= stages) mbar_wait_parity_sleep(&empty[s], (uint32_t)(k / stages - 1) & 1u);
+        // stage row 0 holds image row r0-1 (absent for the top band); rows
+        // that do not exist are never read
+        const int64_t img = u / bands;
+        const int r0 = (int)(u - img * bands) * band;
+        const int rs = max(r0 - 1, 0);
+        const int re = min(r0 + band, H - 1);
+        const uint32_t bytes = (uint32_t)(re - rs + 1) * (uint32_t)W * 4u;
+        float* dst = in_buf + (size_t)s * in_stage + (size_t)(rs - (r0 - 1)) * W;
+        const float* src = depth + ((size_t)img * H + rs) * (size_t)W;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(dst, src, bytes, &full[s]);
+      }
     }
+    return;
+  }
+  if (warp == cons_warps + 1) {
+    // ---------------------------------------------------------- storer ---
+    if (U8) {
+      int k = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int b = k & 1;
+        mbar_wait_parity_sleep(&ready[b], (uint32_t)(k >> 1) & 1u);
+        const int64_t img = u / bands;
+        const int r0 = (int)(u - img * bands) * band;
+        const uint32_t bytes = (uint32_t)min(band, H - r0) * (uint32_t)W * 3u;
+        uint8_t* dst = out_u8 + ((size_t)img * H + r0) * (size_t)W * 3;
+        const uint8_t* ob = out_buf + (size_t)b * out_stage;
+        if (bulk_store & 1) {
+          if (lane == 0) {
+            bulk_s2g(dst, ob, bytes);
+            bulk_commit();
+            bulk_wait_read<1>();  // the store of tile k-1 has left shared memory
+            if (k >= 1) mbar_arrive(&ofree[b ^ 1]);
+          }
+        } else {
+          const uint32_t* s32 = reinterpret_cast<const uint32_t*>(ob);
+          uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+          for (uint32_t i = lane; i < bytes / 4; i += 32) d32[i] = s32[i];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ofree[b]);
+        }
+      }
+      if ((bulk_store & 1) && lane == 0) bulk_wait_all<0>();
+    }
+    return;
   }
 
-  int it = 0;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-    const int s = it % stages;
-    const uint32_t parity = (uint32_t)(it / stages) & 1u;
-    const int64_t img = u / bands;
-    const int r0 = (int)(u - img * bands) * band;
-    const int nrows = min(band, H - r0);
-    uint8_t* ob = out_buf + (size_t)(it & 1) * out_stage;
-    if (U8 && bulk_store && threadIdx.x == 0) bulk_wait_read<1>();  // store of it-2 has left `ob`
-    __syncthreads();
-    mbar_wait_parity(&bars[s], parity);
+  // ------------------------------------------------------------ consumers ---
+  // per-thread constants: column quad, row group (padding lanes of a partial
+  // last warp get an out-of-band group and only take part in the handshakes)
+  const bool is_cons = (int)threadIdx.x < n_cons;
+  const int xq = threadIdx.x % QW;
+  const int g = is_cons ? (int)threadIdx.x / QW : groups;
+  const int x0 = xq << 2;
+  const bool at_left = (x0 == 0), at_right = (x0 + 4 >= W);
+  const float m0 = at_left ? 2.f : 1.f;  // np.gradient one-sided borders are not halved:
+  const float m3 = at_right ? 2.f : 1.f; // h = 2*(f1-f0) in the doubled-gradient form
+  const int lr0 = g * RPT;
+  const size_t row_off = (size_t)lr0 * W + x0;   // this thread's first pixel inside a band
 
-    const float* tile = in_buf + (size_t)s * in_stage + W;  // tile row lr = image row r0 + lr
-    const int lr0 = g * RPT;
-    if (lr0 < nrows) {
-      // register window: win[k] = image row r0 + lr0 - 1 + k; a missing row
-      // (above the image / below it) repeats its neighbour, which together
-      // with the x2 below gives np.gradient's one-sided border rows
-      const float* col = tile + (size_t)lr0 * W + x0;
-      float4 win[RPT + 2];
-      win[1] = *reinterpret_cast<const float4*>(col);
-      win[0] = (r0 + lr0 > 0) ? *reinterpret_cast<const float4*>(col - W) : win[1];
-#pragma unroll
-      for (int k = 1; k <= RPT; ++k)
-        win[k + 1] = (r0 + lr0 + k <= H - 1) ? *reinterpret_cast<const float4*>(col + (size_t)k * W) : win[k];
-      float hl[RPT], hr[RPT];
+  // unit bookkeeping without divisions in the loop
+  const int64_t g_img = gridDim.x / bands;
+  const int g_band = (int)(gridDim.x - g_img * bands);
+  int64_t img = blockIdx.x / bands;
+  int bidx = (int)(blockIdx.x - img * bands);
+  int s = 0, k = 0;
+  uint32_t full_phase = 0;
+  for (; img < n_images; ++k) {
+    const int r0 = bidx * band;
+    const int nrows = min(band, H - r0);
+    const int b = k & 1;
+    const bool active = lr0 < nrows;
+    mbar_wait_parity(&full[s], full_phase);
+    if (U8 && k >= 2) mbar_wait_parity(&ofree[b], (uint32_t)((k >> 1) - 1) & 1u);
+    if (active) {
+      // rolling row window up / c / dn; a missing row (above or below the
+      // image) repeats its neighbour, which with the x2 below gives
+      // np.gradient's one-sided border rows
+      const float* p = in_buf + (size_t)s * in_stage + W + row_off;  // image row r0 + lr0
+      uint32_t* op = reinterpret_cast<uint32_t*>(out_buf + (size_t)b * out_stage + row_off * 3);
+      float* of = F32 ? out_f32 + (((size_t)img * H + r0) * W + row_off) * 3 : nullptr;
+      float4 c = *reinterpret_cast<const float4*>(p);
+      float4 up = (r0 + lr0 > 0) ? *reinterpret_cast<const float4*>(p - W) : c;
 #pragma unroll
       for (int j = 0; j < RPT; ++j) {
-        const float* row = tile + (size_t)(lr0 + j) * W;
-        hl[j] = row[left_off];
-        hr[j] = row[right_off];
-      }
-#pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int lr = lr0 + j;
-        if (lr >= nrows) break;
-        const int r = r0 + lr;
-        const float4 up = win[j], c = win[j + 1], dn = win[j + 2];
-        const float left = hl[j], right = hr[j];
+        if (lr0 + j >= nrows) break;
+        const int r = r0 + lr0 + j;
+        const float4 dn = (r < H - 1) ? *reinterpret_cast<const float4*>(p + W) : c;
+        // left/right neighbours of the quad; the reads at the image's side
+        // borders land inside the stage buffer and are replaced by c.x / c.w
+        const float left = at_left ? c.x : p[-1];
+        const float right = at_right ? c.w : p[4];
         // doubled gradients h = 2g (coefficients carry the 2^-(i+j))
         float2 hy01 = __fadd2_rn(make_float2(dn.x, dn.y), make_float2(-up.x, -up.y));
         float2 hy23 = __fadd2_rn(make_float2(dn.z, dn.w), make_float2(-up.z, -up.w));
@@ -207,64 +258,66 @@ __global__ void __launch_bounds__(kMaxThreads, 2) rgb_bulk_kernel(const float* _
         }
         const float2 hx01 = make_float2((c.y - left) * m0, c.z - c.x);
         const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
-        const float2 r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
-        const float2 g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
-        const float2 b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
-        const float2 r23 = poly2_sat<DEG>(L.c[0], hx23, hy23);
-        const float2 g23 = poly2_sat<DEG>(L.c[1], hx23, hy23);
-        const float2 b23 = poly2_sat<DEG>(L.c[2], hx23, hy23);
-        if (U8) {
-          // pixel order p0..p3, channel-interleaved: (r0 g0 b0 r1)(g1 b1 r2 g2)(b2 r3 g3 b3)
-          const float2 qa = q8x2(make_float2(r01.x, g01.x));
-          const float2 qb = q8x2(make_float2(b01.x, r01.y));
-          const float2 qc = q8x2(make_float2(g01.y, b01.y));
-          const float2 qd = q8x2(make_float2(r23.x, g23.x));
-          const float2 qe = q8x2(make_float2(b23.x, r23.y));
-          const float2 qf = q8x2(make_float2(g23.y, b23.y));
-          const uint32_t w0 = __byte_perm(__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040),
-                                          __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040),
-                                          0x5410);
-          const uint32_t w1 = __byte_perm(__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040),
-                                          __byte_perm(__float_as_uint(qd.x), __float_as_uint(qd.y), 0x0040),
-                                          0x5410);
-          const uint32_t w2 = __byte_perm(__byte_perm(__float_as_uint(qe.x), __float_as_uint(qe.y), 0x0040),
-                                          __byte_perm(__float_as_uint(qf.x), __float_as_uint(qf.y), 0x0040),
-                                          0x5410);
-          uint32_t* o = reinterpret_cast<uint32_t*>(ob + ((size_t)lr * W + x0) * 3);
-          o[0] = w0;
-          o[1] = w1;
-          o[2] = w2;
+        if (bulk_store & 2) {  // TACSL_RGB_DEBUG_COPY: data movement only (roofline experiments)
+          if (U8) {
+            op[0] = __float_as_uint(hx01.x);
+            op[1] = __float_as_uint(hy01.y);
+            op[2] = __float_as_uint(hx23.y);
+          }
+        } else {
+          const float2 r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
+          const float2 g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
+          const float2 b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
+          const float2 r23 = poly2_sat<DEG>(L.c[0], hx23, hy23);
+          const float2 g23 = poly2_sat<DEG>(L.c[1], hx23, hy23);
+          const float2 b23 = poly2_sat<DEG>(L.c[2], hx23, hy23);
+          if (U8) {
+            // pixel order p0..p3, channel-interleaved: (r0 g0 b0 r1)(g1 b1 r2 g2)(b2 r3 g3 b3)
+            const float2 qa = q8x2(make_float2(r01.x, g01.x));
+            const float2 qb = q8x2(make_float2(b01.x, r01.y));
+            const float2 qc = q8x2(make_float2(g01.y, b01.y));
+            const float2 qd = q8x2(make_float2(r23.x, g23.x));
+            const float2 qe = q8x2(make_float2(b23.x, r23.y));
+            const float2 qf = q8x2(make_float2(g23.y, b23.y));
+            op[0] = __byte_perm(__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040),
+                                __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040), 0x5410);
+            op[1] = __byte_perm(__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040),
+                                __byte_perm(__float_as_uint(qd.x), __float_as_uint(qd.y), 0x0040), 0x5410);
+            op[2] = __byte_perm(__byte_perm(__float_as_uint(qe.x), __float_as_uint(qe.y), 0x0040),
+                                __byte_perm(__float_as_uint(qf.x), __float_as_uint(qf.y), 0x0040), 0x5410);
+          }
+          if (F32) {
+            float4* o = reinterpret_cast<float4*>(of);
+            o[0] = make_float4(r01.x, g01.x, b01.x, r01.y);
+            o[1] = make_float4(g01.y, b01.y, r23.x, g23.x);
+            o[2] = make_float4(b23.x, r23.y, g23.y, b23.y);
+            of += (size_t)W * 3;
+          }
         }
-        if (F32) {
-          float4* o = reinterpret_cast<float4*>(out_f32 + (((size_t)img * H + r) * W + x0) * 3);
-          o[0] = make_float4(r01.x, g01.x, b01.x, r01.y);
-          o[1] = make_float4(g01.y, b01.y, r23.x, g23.x);
-          o[2] = make_float4(b23.x, r23.y, g23.y, b23.y);
-        }
+        up = c;
+        c = dn;
+        p += W;
+        op += (W * 3) >> 2;
       }
     }
-    if (U8) fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp no longer reads stage s
     if (U8) {
-      uint8_t* dst = out_u8 + ((size_t)img * H + r0) * (size_t)W * 3;
-      const uint32_t bytes = (uint32_t)nrows * (uint32_t)W * 3u;
-      if (bulk_store) {
-        if (threadIdx.x == 0) {
-          bulk_s2g(dst, ob, bytes);
-          bulk_commit();
-        }
-      } else {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(ob);
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-        for (uint32_t k = threadIdx.x; k < bytes / 4; k += blockDim.x) d32[k] = src[k];
-      }
+      fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[b]);
     }
-    if (threadIdx.x == 0) {
-      const int64_t un = u + (int64_t)stages * gridDim.x;
-      if (un < units) issue(un, s);
+    if (++s == stages) {
+      s = 0;
+      full_phase ^= 1u;
+    }
+    img += g_img;
+    bidx += g_band;
+    if (bidx >= bands) {
+      bidx -= bands;
+      ++img;
     }
   }
-  if (U8 && bulk_store && threadIdx.x == 0) bulk_wait_all<0>();
 }
 
 // Generic path (any W >= 2, any alignment): one thread per pixel, neighbours
@@ -316,27 +369,41 @@ int env_int(const char* name, int dflt) {
 Layout choose_layout(int H, int W, bool u8) {
   const int QW = W / 4;
   Layout lay;
-  lay.rpt = RPT;
-  int groups = env_int("TACSL_RGB_GROUPS", std::max(1, std::min(kMaxThreads / QW, 320 / QW > 0 ? 320 / QW : 1)));
+  lay.rpt = env_int("TACSL_RGB_RPT", kDefaultRpt) == 4 ? 4 : 8;
+  // Defaults measured on B200 at 240x320 (tools/sweep_rgb.py): 8 rows per
+  // thread, 3 row groups (24-row bands), a 2-deep input ring -> 113 KB of
+  // shared memory, two CTAs per SM.
+  const bool user_groups = std::getenv("TACSL_RGB_GROUPS") != nullptr;
+  int groups = env_int("TACSL_RGB_GROUPS", 3);
   groups = std::max(1, std::min(groups, kMaxThreads / QW));
   // no point in more groups than the image has rows
   while (groups > 1 && (groups - 1) * lay.rpt >= H) --groups;
-  lay.groups = groups;
-  lay.band = groups * lay.rpt;
-  lay.stages = env_int("TACSL_RGB_STAGES", 3);
-  lay.in_stage_floats = (size_t)(lay.band + 2) * W;
-  lay.out_stage_bytes = (size_t)lay.band * W * 3;
-  (void)u8;
+  lay.stages = std::max(1, std::min(env_int("TACSL_RGB_STAGES", 2), kMaxStages));
+  auto fill = [&]() {
+    lay.groups = groups;
+    lay.band = groups * lay.rpt;
+    lay.in_stage_floats = (size_t)(lay.band + 2) * W;
+    lay.out_stage_bytes = (size_t)lay.band * W * 3;
+  };
+  fill();
+  // shrink the band until two CTAs share an SM (default) or one CTA fits
+  const size_t target = user_groups ? kSmemPerSm : kSmemPerSm / 2;
+  while (groups > 1 && lay.bytes(u8) > target) {
+    --groups;
+    fill();
+  }
+  while (lay.stages > 1 && lay.bytes(u8) > kSmemPerSm) {
+    --lay.stages;
+  }
   return lay;
 }
 
-template <int DEG, bool U8, bool F32>
-int launch_bulk(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32, const LutParams& L,
-                cudaStream_t stream) {
-  Layout lay = choose_layout(H, W, U8);
-  const int threads = (W / 4) * lay.groups;
+template <int DEG, int RPT, bool U8, bool F32>
+int launch_bulk(const Layout& lay, const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32,
+                const LutParams& L, cudaStream_t stream) {
+  const int threads = (((W / 4) * lay.groups + 31) / 32) * 32 + 64;  // consumer warps + loader + storer
   size_t smem = lay.bytes(U8);
-  auto kern = rgb_bulk_kernel<DEG, U8, F32>;
+  auto kern = rgb_bulk_kernel<DEG, RPT, U8, F32>;
   static std::mutex mu;
   static size_t configured = 0;
   {
@@ -354,8 +421,10 @@ int launch_bulk(const float* depth, int64_t n, int H, int W, uint8_t* u8, float*
   const int bands = (H + lay.band - 1) / lay.band;
   const int64_t units = n * bands;
   int64_t grid = std::min<int64_t>(units, (int64_t)sm_count(current_device()) * per_sm);
-  const int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
-  kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.stages, u8, f32, L, bulk_store);
+  int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
+  if (std::getenv("TACSL_RGB_DEBUG_COPY")) bulk_store |= 2;
+  kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
+                                                  bulk_store);
   return check_launch("rgb_bulk_kernel");
 }
 
@@ -366,9 +435,15 @@ int dispatch(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f3
                        ((reinterpret_cast<uintptr_t>(depth) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(f32) & 15) == 0) && ((reinterpret_cast<uintptr_t>(u8) & 3) == 0);
   if (aligned && !std::getenv("TACSL_RGB_FORCE_SCALAR")) {
-    if (u8 && f32) return launch_bulk<DEG, true, true>(depth, n, H, W, u8, f32, L, stream);
-    if (u8) return launch_bulk<DEG, true, false>(depth, n, H, W, u8, f32, L, stream);
-    return launch_bulk<DEG, false, true>(depth, n, H, W, u8, f32, L, stream);
+    const Layout lay = choose_layout(H, W, u8 != nullptr);
+    if (lay.rpt == 4) {
+      if (u8 && f32) return launch_bulk<DEG, 4, true, true>(lay, depth, n, H, W, u8, f32, L, stream);
+      if (u8) return launch_bulk<DEG, 4, true, false>(lay, depth, n, H, W, u8, f32, L, stream);
+      return launch_bulk<DEG, 4, false, true>(lay, depth, n, H, W, u8, f32, L, stream);
+    }
+    if (u8 && f32) return launch_bulk<DEG, 8, true, true>(lay, depth, n, H, W, u8, f32, L, stream);
+    if (u8) return launch_bulk<DEG, 8, true, false>(lay, depth, n, H, W, u8, f32, L, stream);
+    return launch_bulk<DEG, 8, false, true>(lay, depth, n, H, W, u8, f32, L, stream);
   }
   const int64_t total = n * (int64_t)H * W;
   int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(current_device()) * 16);

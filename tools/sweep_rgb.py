@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--stages", default="2,3,4")
     ap.add_argument("--ctas", default="1,2")
     ap.add_argument("--f32", action="store_true")
+    ap.add_argument("--rpt", default="4,8")
     a = ap.parse_args()
     W, H = (int(v) for v in a.size.split("x"))
     _, cam, bg, _, _ = synthetic.sensor_setup((W, H))
@@ -40,7 +41,9 @@ def main():
     QW = W // 4
     groups = [int(g) for g in a.groups.split(",")] if a.groups else sorted({g for g in (1, 2, 3, 4, 5, 6) if QW * g <= 384})
     results = []
-    for g, st, c in itertools.product(groups, [int(v) for v in a.stages.split(",")], [int(v) for v in a.ctas.split(",")]):
+    for rpt, g, st, c in itertools.product([int(v) for v in a.rpt.split(",")], groups,
+                                           [int(v) for v in a.stages.split(",")], [int(v) for v in a.ctas.split(",")]):
+        os.environ["TACSL_RGB_RPT"] = str(rpt)
         os.environ["TACSL_RGB_GROUPS"] = str(g)
         os.environ["TACSL_RGB_STAGES"] = str(st)
         os.environ["TACSL_RGB_CTAS_PER_SM"] = str(c)
@@ -49,7 +52,7 @@ def main():
                 render.depth_to_rgb_device(depth, lut, out_u8=u8, out_f32=f32)
             torch.cuda.synchronize()
         except Exception as e:  # noqa: BLE001
-            print(json.dumps({"groups": g, "stages": st, "ctas": c, "error": str(e)}))
+            print(json.dumps({"rpt": rpt, "groups": g, "stages": st, "ctas": c, "error": str(e)}))
             continue
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
@@ -58,7 +61,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
-        r = {"groups": g, "stages": st, "ctas": c, "ms": round(ms, 4), "GBps": round(bytes_ / ms / 1e6, 1)}
+        r = {"rpt": rpt, "groups": g, "stages": st, "ctas": c, "ms": round(ms, 4), "GBps": round(bytes_ / ms / 1e6, 1)}
         results.append(r)
         print(json.dumps(r), flush=True)
     best = max(results, key=lambda r: r["GBps"])

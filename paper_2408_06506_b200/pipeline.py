@@ -109,6 +109,62 @@ class SensorArray:
     # kernels launched per step (for the bench's gpu_launches count)
     launches_per_step = 2
 
+    def host_buffers(self, pinned=True):
+        """Pinned host mirrors of the step's inputs and outputs."""
+        t = _device.torch()
+
+        def like(shape, dtype):
+            return t.empty(shape, dtype=dtype, pin_memory=pinned)
+
+        W, H = self.W, self.H
+        return {
+            "depth": like((self.E, self.S, H, W), t.float32),
+            "obj": like((self.E, 13), t.float64),
+            "sen": like((self.E, self.S, 13), t.float64),
+            "rgb": like(tuple(self.rgb_u8.shape), t.uint8) if self.rgb_u8 is not None else None,
+            "f_n": like(tuple(self.f_n.shape), self.f_n.dtype),
+            "f_t": like(tuple(self.f_t.shape), self.f_t.dtype),
+            "wrench": like(tuple(self.wrench.shape), t.float64),
+        }
+
+    def run_host(self, host, depth, obj_state, sen_state, chunks=8):
+        """One step from pinned HOST inputs to pinned HOST outputs.
+
+        The env axis is cut into `chunks`; chunk i's host->device copy, chunk
+        i-1's kernels and chunk i-2's device->host copy run concurrently on
+        three streams (two copy engines + the SMs), so a step costs about the
+        larger of the two PCIe directions rather than their sum.  `depth`,
+        `obj_state`, `sen_state` are the device staging tensors.
+        """
+        t = _device.torch()
+        dev = self.device
+        if not hasattr(self, "_h2d"):
+            self._h2d = t.cuda.Stream(device=dev)
+            self._d2h = t.cuda.Stream(device=dev)
+        main = t.cuda.current_stream(dev)
+        self._h2d.wait_stream(main)
+        bounds = [shard_range(self.E, i, chunks) for i in range(chunks)]
+        bounds = [(lo, hi) for lo, hi in bounds if hi > lo]
+        outs = [("rgb", self.rgb_u8), ("f_n", self.f_n), ("f_t", self.f_t), ("wrench", self.wrench)]
+        for lo, hi in bounds:
+            with t.cuda.stream(self._h2d):
+                depth[lo:hi].copy_(host["depth"][lo:hi], non_blocking=True)
+                obj_state[lo:hi].copy_(host["obj"][lo:hi], non_blocking=True)
+                sen_state[lo:hi].copy_(host["sen"][lo:hi], non_blocking=True)
+            main.wait_stream(self._h2d)
+            depth_to_rgb_device(depth[lo:hi], self.lut, out_u8=None if self.rgb_u8 is None else self.rgb_u8[lo:hi],
+                                out_f32=None if self.rgb_f32 is None else self.rgb_f32[lo:hi])
+            force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state[lo:hi], sen_state[lo:hi],
+                               self.params, self.f_n[lo:hi], self.f_t[lo:hi], wrench=self.wrench[lo:hi],
+                               n_sensors=self.S, obj_stride=13, sen_stride=13 * self.S)
+            self._d2h.wait_stream(main)
+            with t.cuda.stream(self._d2h):
+                for name, dev_t in outs:
+                    if dev_t is not None and host.get(name) is not None:
+                        host[name][lo:hi].copy_(dev_t[lo:hi], non_blocking=True)
+        main.wait_stream(self._d2h)
+        return host
+
 
 def shard_range(n_envs: int, rank: int, world: int):
     """Contiguous env shard [lo, hi) of `rank`."""

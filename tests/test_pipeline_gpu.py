@@ -75,3 +75,25 @@ def test_cuda_graph_replay_matches_eager():
     for a, b in zip(eager, (arr.rgb_u8, arr.f_n, arr.f_t, arr.wrench)):
         assert torch.equal(a, b)
     assert torch.equal(rgb_rev, eager[0].flip(0))
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_run_host_pipelined_matches_device_step(chunks):
+    lut, pts, sdf, depth, obj, sen = setup(E=10)
+    E, S = sen.shape[:2]
+    arr = SensorArray(lut, sdf, pts, PenaltyParams(), E, S)
+    d = torch.from_numpy(depth).cuda()
+    o = torch.from_numpy(obj).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(sen)).cuda()
+    arr.launch(d, o, s)
+    torch.cuda.synchronize()
+    ref = [x.cpu() for x in (arr.rgb_u8, arr.f_n, arr.f_t, arr.wrench)]
+    host = arr.host_buffers()
+    host["depth"].copy_(torch.from_numpy(depth))
+    host["obj"].copy_(torch.from_numpy(obj))
+    host["sen"].copy_(torch.from_numpy(np.ascontiguousarray(sen)))
+    d.zero_()
+    arr.run_host(host, d, o, s, chunks=chunks)
+    torch.cuda.synchronize()
+    for name, r in zip(("rgb", "f_n", "f_t", "wrench"), ref):
+        assert torch.equal(host[name], r), name

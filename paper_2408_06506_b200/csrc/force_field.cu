@@ -21,8 +21,9 @@
 //
 // Mapping: one CTA per sensor frame (env e, sensor s); threads stride over the
 // rows*cols taxels.  The SDF is a float64 {d, gx, gy, gz} grid (32 B per cell,
-// two 16B loads per trilinear corner) that stays L2-resident (2 MiB for the
-// 32x32x64 peg, 64 MiB at 128^3).
+// one 256-bit load per trilinear corner) that stays L2-resident (2 MiB for
+// the 32x32x64 peg, 64 MiB at 128^3).  Out of contact both forces are exactly
+// zero, so only contact taxels pay for the normal, velocities and penalty law.
 #include <algorithm>
 
 #include "common.cuh"

@@ -22,6 +22,7 @@
  *                           (+ net_wrench tactile/field.py:132-141 fused as a
  *                           per-sensor reduction when `wrench` is non-NULL)
  *   tacsl_net_wrench        tactile/field.py:132-141 net_wrench (standalone)
+ *   tacsl_render_depth      render/depth.py:88-134 render_depth (SDF sphere tracer)
  *
  * The reference has no FFI of its own (pure numpy); the Python module
  * paper_2408_06506_b200 binds these with ctypes behind the reference's
@@ -115,6 +116,26 @@ TACSL_API void tacsl_sdf_destroy(tacsl_sdf_t sdf);
 TACSL_API int tacsl_query_sdf(tacsl_sdf_t sdf, const double* points, int64_t n,
                     double* distance, double* normal, uint8_t* valid,
                     void* stream);
+
+/* ------------------------------------------------------- depth render --- */
+/* Sphere-traced in-sensor depth (render/depth.py:88-134, numba march
+ * depth.py:174-233), bit-identical to the reference in float64.
+ *   dirs        (H*W, 3) float64 unit ray directions, sensor frame
+ *               (TactileCamera.rays, camera.py:36-43)
+ *   background  (H*W) float64 membrane depth (reference_depth, camera.py:56-66)
+ *   cam_pos     HOST double[3], camera position in the sensor frame
+ *   env_params  (E, 18) float64 per env: object pos[3], R[9] (object->sensor,
+ *               row-major, quat_to_mat of the object quaternion,
+ *               transforms.py:78-91), the object's grid-box AABB lo[3], hi[3]
+ *               in the sensor frame (depth.py:107-112)
+ *   depth_f64 / depth_f32  nullable (E, H, W) outputs (not both NULL)
+ * hit_tolerance / max_steps: HIT_TOLERANCE = 2e-5, MAX_STEPS = 64
+ * (depth.py:18-19) in the reference. */
+TACSL_API int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const double* background,
+                                 int height, int width, const double cam_pos[3], double near_plane,
+                                 double far_plane, double hit_tolerance, int max_steps,
+                                 const double* env_params, int64_t n_envs, double* depth_f64,
+                                 float* depth_f32, void* stream);
 
 /* -------------------------------------------------------- force field --- */
 /* Elementwise penalty formulas on `count` points, all float64:

@@ -117,16 +117,21 @@ int tacsl_sdf_create(int device, const double* values, const double* gradients, 
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   double4* dptr = nullptr;
+  double* vptr = nullptr;
   cudaError_t e = cudaMalloc(&dptr, n * sizeof(double4));
+  if (e == cudaSuccess) e = cudaMalloc(&vptr, n * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(dptr, host.data(), n * sizeof(double4), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(vptr, values, n * sizeof(double), cudaMemcpyHostToDevice);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     if (dptr) cudaFree(dptr);
+    if (vptr) cudaFree(vptr);
     return set_error(TACSL_ERR_CUDA, std::string("sdf_create: ") + cudaGetErrorString(e));
   }
   auto* h = new tacsl_sdf_s();
   h->device = device;
   h->grid = dptr;
+  h->values = vptr;
   for (int a = 0; a < 3; ++a) {
     h->dims[a] = dims[a];
     h->origin[a] = origin[a];
@@ -142,6 +147,7 @@ void tacsl_sdf_destroy(tacsl_sdf_t sdf) {
   cudaGetDevice(&prev);
   cudaSetDevice(sdf->device);
   cudaFree(sdf->grid);
+  cudaFree(sdf->values);
   cudaSetDevice(prev);
   delete sdf;
 }

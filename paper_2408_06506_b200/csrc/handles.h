@@ -25,7 +25,8 @@ struct tacsl_lut_s {
 
 struct tacsl_sdf_s {
   int device;
-  double4* grid;  // (nx, ny, nz) {d, gx, gy, gz}, z fastest, 32 B per cell
+  double4* grid;   // (nx, ny, nz) {d, gx, gy, gz}, z fastest, 32 B per cell (force field)
+  double* values;  // (nx, ny, nz) d only, 8 B per cell (sphere tracing)
   int dims[3];
   double origin[3];
   double spacing;

@@ -1,0 +1,162 @@
+// K3: in-sensor depth rendering by sphere tracing the object's SDF.
+//
+// Replaces render/depth.py:88-134 render_depth: per pixel ray, slab-test the
+// object's rotated grid box (_ray_aabb, depth.py:77-85), march from
+// max(t_in, near) towards min(background, t_out) with step = trilinear SDF
+// value inside the grid and the distance to the grid box outside it, record
+// the first t with d < HIT_TOLERANCE, keep min(hit, membrane) and clip to
+// [near, far].  The march mirrors the reference's numba kernel
+// (_march_kernel, depth.py:174-233) operation for operation in float64 with
+// separately rounded products and sums (numba/numpy never contract to FMA),
+// so the depth map is bit-identical to the reference's.
+//
+// Mapping: one thread per (env, pixel) ray; consecutive threads walk
+// consecutive pixels of one env, so a warp's rays hit neighbouring cells of
+// the L2-resident float64 value grid (8 B per cell).
+#include <algorithm>
+
+#include "common.cuh"
+#include "handles.h"
+
+namespace tacsl {
+namespace {
+
+struct RenderParams {
+  const double* __restrict__ values;  // (nx, ny, nz) float64, z fastest
+  int nx, ny, nz;
+  double gox, goy, goz, spacing;
+  double hix, hiy, hiz;  // origin + spacing * (dims - 1)  (depth.py:180-182)
+  double cx, cy, cz;     // camera position (sensor frame)
+  double near_, far_, tol;
+  int max_steps;
+  int n_rays;
+};
+
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }  // np.maximum w/o NaNs
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+
+__global__ void __launch_bounds__(256) render_depth_kernel(const RenderParams P, const double* __restrict__ dirs,
+                                                           const double* __restrict__ background,
+                                                           const double* __restrict__ envp, int64_t n_envs,
+                                                           double* __restrict__ out64, float* __restrict__ out32) {
+  const int64_t total = n_envs * (int64_t)P.n_rays;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int64_t e = idx / P.n_rays;
+    const int r = (int)(idx - e * P.n_rays);
+    const double* ep = envp + e * 18;  // pos[3], rot[9] (object->sensor, row-major), lo[3], hi[3]
+    const double dx = __ldg(dirs + 3 * r), dy = __ldg(dirs + 3 * r + 1), dz = __ldg(dirs + 3 * r + 2);
+    const double bg = __ldg(background + r);
+
+    // ---- slab test (depth.py:77-85) ----
+    const double ivx = 1.0 / (fabs(dx) < 1e-300 ? 1e-300 : dx);
+    const double ivy = 1.0 / (fabs(dy) < 1e-300 ? 1e-300 : dy);
+    const double ivz = 1.0 / (fabs(dz) < 1e-300 ? 1e-300 : dz);
+    const double t0x = mul_rn(sub_rn(__ldg(ep + 12), P.cx), ivx), t1x = mul_rn(sub_rn(__ldg(ep + 15), P.cx), ivx);
+    const double t0y = mul_rn(sub_rn(__ldg(ep + 13), P.cy), ivy), t1y = mul_rn(sub_rn(__ldg(ep + 16), P.cy), ivy);
+    const double t0z = mul_rn(sub_rn(__ldg(ep + 14), P.cz), ivz), t1z = mul_rn(sub_rn(__ldg(ep + 17), P.cz), ivz);
+    const double tmin = dmax(dmax(dmin(t0x, t1x), dmin(t0y, t1y)), dmin(t0z, t1z));
+    const double tmax = dmin(dmin(dmax(t0x, t1x), dmax(t0y, t1y)), dmax(t0z, t1z));
+    const bool hit_box = tmax >= dmax(tmin, 0.0);
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    const double t_in = hit_box ? dmax(tmin, 0.0) : inf;
+    const double t_out = hit_box ? tmax : -inf;
+    const double t_stop = dmin(bg, t_out);
+    const double t_start = dmax(t_in, P.near_);
+    double depth = bg;
+
+    if (t_start <= t_stop) {
+      // ---- sphere trace (depth.py:183-233) ----
+      const double px = __ldg(ep + 0), py = __ldg(ep + 1), pz = __ldg(ep + 2);
+      const double r00 = __ldg(ep + 3), r01 = __ldg(ep + 4), r02 = __ldg(ep + 5);
+      const double r10 = __ldg(ep + 6), r11 = __ldg(ep + 7), r12 = __ldg(ep + 8);
+      const double r20 = __ldg(ep + 9), r21 = __ldg(ep + 10), r22 = __ldg(ep + 11);
+      double t = t_start;
+      for (int step = 0; step < P.max_steps; ++step) {
+        const double wx = sub_rn(add_rn(P.cx, mul_rn(dx, t)), px);
+        const double wy = sub_rn(add_rn(P.cy, mul_rn(dy, t)), py);
+        const double wz = sub_rn(add_rn(P.cz, mul_rn(dz, t)), pz);
+        // R^T w: sensor -> object frame
+        const double ox = add_rn(add_rn(mul_rn(r00, wx), mul_rn(r10, wy)), mul_rn(r20, wz));
+        const double oy = add_rn(add_rn(mul_rn(r01, wx), mul_rn(r11, wy)), mul_rn(r21, wz));
+        const double oz = add_rn(add_rn(mul_rn(r02, wx), mul_rn(r12, wy)), mul_rn(r22, wz));
+        double d;
+        if (ox < P.gox || oy < P.goy || oz < P.goz || ox > P.hix || oy > P.hiy || oz > P.hiz) {
+          // outside the grid: distance to the box is a safe step (depth.py:205-210)
+          const double bx = add_rn(dmax(sub_rn(P.gox, ox), 0.0), dmax(sub_rn(ox, P.hix), 0.0));
+          const double by = add_rn(dmax(sub_rn(P.goy, oy), 0.0), dmax(sub_rn(oy, P.hiy), 0.0));
+          const double bz = add_rn(dmax(sub_rn(P.goz, oz), 0.0), dmax(sub_rn(oz, P.hiz), 0.0));
+          d = dmax(__dsqrt_rn(add_rn(add_rn(mul_rn(bx, bx), mul_rn(by, by)), mul_rn(bz, bz))), P.spacing);
+        } else {
+          const double gx = __ddiv_rn(sub_rn(ox, P.gox), P.spacing);
+          const double gy = __ddiv_rn(sub_rn(oy, P.goy), P.spacing);
+          const double gz = __ddiv_rn(sub_rn(oz, P.goz), P.spacing);
+          const int ix = min((int)gx, P.nx - 2), iy = min((int)gy, P.ny - 2), iz = min((int)gz, P.nz - 2);
+          const double fx = sub_rn(gx, (double)ix), fy = sub_rn(gy, (double)iy), fz = sub_rn(gz, (double)iz);
+          const double ux = sub_rn(1.0, fx), uy = sub_rn(1.0, fy), uz = sub_rn(1.0, fz);
+          const size_t sy = (size_t)P.nz, sx = (size_t)P.ny * P.nz;
+          const double* v = P.values + (size_t)ix * sx + (size_t)iy * sy + iz;
+          const double c00 = add_rn(mul_rn(__ldg(v), ux), mul_rn(__ldg(v + sx), fx));
+          const double c10 = add_rn(mul_rn(__ldg(v + sy), ux), mul_rn(__ldg(v + sx + sy), fx));
+          const double c01 = add_rn(mul_rn(__ldg(v + 1), ux), mul_rn(__ldg(v + sx + 1), fx));
+          const double c11 = add_rn(mul_rn(__ldg(v + sy + 1), ux), mul_rn(__ldg(v + sx + sy + 1), fx));
+          const double c0 = add_rn(mul_rn(c00, uy), mul_rn(c10, fy));
+          const double c1 = add_rn(mul_rn(c01, uy), mul_rn(c11, fy));
+          d = add_rn(mul_rn(c0, uz), mul_rn(c1, fz));
+        }
+        if (d < P.tol) {
+          if (t < depth) depth = t;
+          break;
+        }
+        t = add_rn(t, d);
+        if (t > t_stop) break;
+      }
+    }
+    depth = dmin(dmax(depth, P.near_), P.far_);  // np.clip(depth, near, far)
+    if (out64) out64[idx] = depth;
+    if (out32) out32[idx] = (float)depth;
+  }
+}
+
+}  // namespace
+}  // namespace tacsl
+
+using namespace tacsl;
+
+extern "C" int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const double* background, int height,
+                                  int width, const double cam_pos[3], double near_plane, double far_plane,
+                                  double hit_tolerance, int max_steps, const double* env_params, int64_t n_envs,
+                                  double* depth_f64, float* depth_f32, void* stream) {
+  if (!sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "render_depth: null SDF");
+  if (height <= 0 || width <= 0 || n_envs < 0 || max_steps < 0)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "render_depth: bad sizes");
+  if (!(near_plane > 0 && near_plane < far_plane)) return set_error(TACSL_ERR_INVALID_ARGUMENT, "need 0 < near < far");
+  if (n_envs == 0) return TACSL_OK;
+  if (!dirs || !background || !cam_pos || !env_params || (!depth_f64 && !depth_f32))
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "render_depth: null pointer");
+  RenderParams P;
+  P.values = sdf->values;
+  P.nx = sdf->dims[0];
+  P.ny = sdf->dims[1];
+  P.nz = sdf->dims[2];
+  P.gox = sdf->origin[0];
+  P.goy = sdf->origin[1];
+  P.goz = sdf->origin[2];
+  P.spacing = sdf->spacing;
+  P.hix = sdf->origin[0] + sdf->spacing * (double)(P.nx - 1);
+  P.hiy = sdf->origin[1] + sdf->spacing * (double)(P.ny - 1);
+  P.hiz = sdf->origin[2] + sdf->spacing * (double)(P.nz - 1);
+  P.cx = cam_pos[0];
+  P.cy = cam_pos[1];
+  P.cz = cam_pos[2];
+  P.near_ = near_plane;
+  P.far_ = far_plane;
+  P.tol = hit_tolerance;
+  P.max_steps = max_steps;
+  P.n_rays = height * width;
+  const int64_t total = n_envs * (int64_t)P.n_rays;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(current_device()) * 32);
+  render_depth_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(P, dirs, background, env_params, n_envs,
+                                                                          depth_f64, depth_f32);
+  return check_launch("render_depth_kernel");
+}

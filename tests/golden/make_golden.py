@@ -36,6 +36,7 @@ sys.path.insert(0, str(REF_SRC))
 sys.path.insert(0, str(ROOT))
 
 from gelsim.geometry import build_sdf, make_cylinder, query_sdf  # noqa: E402
+from gelsim.render import camera_for_sensor, reference_depth, render_depth  # noqa: E402
 from gelsim.render import DepthImage, PolyLut, depth_to_rgb, synthetic_lut, to_uint8  # noqa: E402
 from gelsim.sensors import TactileSensorSpec  # noqa: E402
 from gelsim.tactile import PenaltyParams, compute_force_field, net_wrench, penalty_forces  # noqa: E402
@@ -168,11 +169,39 @@ def make_penalty():
                         f_n=f_n[sel], f_t=f_t[sel])
 
 
+def make_depth(grid):
+    """render_depth (numba march, render/depth.py:88-134) on the reference
+    peg grid: peg lying across the pad at several presses, one pose out of
+    contact, one arbitrary rotation; 60x80 (E=6) and 240x320 (E=1)."""
+    out = {}
+    for (W, H), E in (((80, 60), 6), ((320, 240), 1)):
+        sensor = TactileSensorSpec(image_size=(W, H))
+        cam = camera_for_sensor(sensor)
+        bg = reference_depth(cam, sensor)
+        obj, sen = synthetic.peg_states(E, 1, config_id=105 + W, random_sensor_pose=False)
+        pos, quat = obj[:, 0:3].copy(), obj[:, 3:7].copy()
+        if E > 2:
+            pos[-1, 2] += 0.01                                   # lifted: no contact
+            quat[-2] = np.array([0.9, 0.2, -0.3, 0.25]) / np.linalg.norm([0.9, 0.2, -0.3, 0.25])
+            pos[-2, 2] = 0.006
+        img = render_depth(cam, grid, pos, quat, bg)
+        key = f"{H}x{W}"
+        out[f"bg_{key}"] = bg
+        out[f"pos_{key}"] = pos
+        out[f"quat_{key}"] = quat
+        out[f"depth_{key}"] = img.values
+    single = render_depth(camera_for_sensor(TactileSensorSpec()), grid, out["pos_60x80"][0], out["quat_60x80"][0],
+                          out["bg_60x80"])
+    out["depth_single"] = single.values
+    np.savez_compressed(HERE / "depth.npz", **out)
+
+
 if __name__ == "__main__":
     make_rgb()
     g = peg_grid_reference()
     make_sdf(g)
     make_ff(g)
     make_penalty()
+    make_depth(g)
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -118,3 +118,15 @@ def test_taxel_layout_bit_exact(golden):
 def test_penalty_params_validation():
     with pytest.raises(ValueError):
         PenaltyParams(k_n=-1.0)
+
+
+@pytest.mark.parametrize("size", [(80, 60), (320, 240)])
+def test_oracle_render_depth_bit_exact(golden, golden_grid, size):
+    from paper_2408_06506_b200.sensors import camera_for_sensor
+    z = golden("depth")
+    W, H = size
+    cam = camera_for_sensor(TactileSensorSpec(image_size=size))
+    k = f"{H}x{W}"
+    got = O.render_depth(cam.rays(), z["bg_" + k], cam.pos, cam.near, cam.far, golden_grid.origin,
+                         golden_grid.spacing, golden_grid.dims, golden_grid.values, z["pos_" + k], z["quat_" + k])
+    assert np.array_equal(got, z["depth_" + k])

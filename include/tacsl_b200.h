@@ -95,6 +95,16 @@ TACSL_API int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n_
                        int height, int width, uint8_t* rgb_u8, float* rgb_f32,
                        void* stream);
 
+/* Policy observation image of envs/peg_tasks.py:434-458 without
+ * augmentation: depth (N, H, W) -> float32 RGB in the env's representation,
+ *   rep 0 "color"  (N, H, W, 3)  rgb                  (peg_tasks.py:445)
+ *   rep 1 "diff"   (N, H, W, 3)  rgb - nominal         (peg_tasks.py:453-454)
+ *   rep 2 "concat" (N, H, W, 6)  [rgb, nominal]        (peg_tasks.py:455-458)
+ * nominal: HOST float[3], the LUT background colour (peg_tasks.py:111-112). */
+TACSL_API int tacsl_tactile_image_obs(tacsl_lut_t lut, const float* depth, int64_t n_images,
+                                      int height, int width, int rep, const float nominal[3],
+                                      float* out, void* stream);
+
 /* x (count) float32 -> u8 = clip(rint(255*x), 0, 255) (imageio.py:8-11). */
 TACSL_API int tacsl_to_uint8(const float* x, int64_t count, uint8_t* out, void* stream);
 
@@ -157,13 +167,16 @@ TACSL_API int tacsl_penalty_forces(const double* d, const double* d_dot, const d
  *   kin           nullable (E, S, R, C, 8) float64 = d, d_dot, v_t[3], n[3]
  *                 (world frame, field.py:123-129)
  *   contact       nullable (E, S, R, C) uint8 = (d < 0) (field.py:64)
+ *   obs           nullable (E, S, R, C, 3) float32 policy observation
+ *                 [f_n.z, f_t.x, f_t.y] (envs/peg_tasks.py:474-476)
+ * f_n / f_t may be NULL when only the wrench / observation is wanted.
  */
 TACSL_API int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
                       const double* object_state, int64_t object_stride,
                       const double* sensor_state, int64_t sensor_stride,
                       int64_t n_envs, int n_sensors, tacsl_penalty_t params,
                       int out_fp64, void* f_n, void* f_t, double* wrench,
-                      double* kin, uint8_t* contact, void* stream);
+                      double* kin, uint8_t* contact, float* obs, void* stream);
 
 /* net_wrench on an existing field: f_n, f_t (frames, rows, cols, 3) float64,
  * points (rows, cols, 3) float64 -> force, torque (frames, 3) float64. */

@@ -36,7 +36,8 @@ SIGNATURES = {
     "tacsl_query_sdf": (c_int, [c_void_p, P, c_int64, P, P, P, c_void_p]),
     "tacsl_penalty_forces": (c_int, [P, P, P, P, c_int64, Penalty, P, P, c_void_p]),
     "tacsl_force_field": (c_int, [c_void_p, P, c_int, c_int, P, c_int64, P, c_int64, c_int64, c_int,
-                                  Penalty, c_int, P, P, P, P, P, c_void_p]),
+                                  Penalty, c_int, P, P, P, P, P, P, c_void_p]),
+    "tacsl_tactile_image_obs": (c_int, [c_void_p, P, c_int64, c_int, c_int, c_int, P, P, c_void_p]),
     "tacsl_net_wrench": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, c_void_p]),
     "tacsl_render_depth": (c_int, [c_void_p, P, P, c_int, c_int, P, c_double, c_double, c_double, c_int, P,
                                    c_int64, P, P, c_void_p]),

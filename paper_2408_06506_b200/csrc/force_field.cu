@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(128, 4) force_field_kernel(
     const Grid grid, const double* __restrict__ taxels, int n_taxels, const double* __restrict__ obj_state,
     int64_t obj_stride, const double* __restrict__ sen_state, int64_t sen_stride, int n_sensors, const Penalty P,
     OutT* __restrict__ f_n_out, OutT* __restrict__ f_t_out, double* __restrict__ wrench, double* __restrict__ kin,
-    uint8_t* __restrict__ contact_out) {
+    uint8_t* __restrict__ contact_out, float* __restrict__ obs_out) {
   const int64_t frame = blockIdx.x;
   const int64_t e = frame / n_sensors;
   const int s = (int)(frame - e * n_sensors);
@@ -288,12 +288,21 @@ __global__ void __launch_bounds__(128, 4) force_field_kernel(
       }
     }
     const int64_t o = (out_base + i) * 3;
-    f_n_out[o + 0] = (OutT)fn.x;
-    f_n_out[o + 1] = (OutT)fn.y;
-    f_n_out[o + 2] = (OutT)fn.z;
-    f_t_out[o + 0] = (OutT)ft.x;
-    f_t_out[o + 1] = (OutT)ft.y;
-    f_t_out[o + 2] = (OutT)ft.z;
+    if (f_n_out) {
+      f_n_out[o + 0] = (OutT)fn.x;
+      f_n_out[o + 1] = (OutT)fn.y;
+      f_n_out[o + 2] = (OutT)fn.z;
+    }
+    if (f_t_out) {
+      f_t_out[o + 0] = (OutT)ft.x;
+      f_t_out[o + 1] = (OutT)ft.y;
+      f_t_out[o + 2] = (OutT)ft.z;
+    }
+    if (obs_out) {  // policy observation [f_n.z, f_t.x, f_t.y] (envs/peg_tasks.py:474-476)
+      obs_out[o + 0] = (float)fn.z;
+      obs_out[o + 1] = (float)ft.x;
+      obs_out[o + 2] = (float)ft.y;
+    }
     if (contact_out) contact_out[out_base + i] = contact ? 1 : 0;
   }
   if (wrench) {
@@ -439,7 +448,7 @@ int tacsl_penalty_forces(const double* d, const double* d_dot, const double* n, 
 int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols, const double* object_state,
                       int64_t object_stride, const double* sensor_state, int64_t sensor_stride, int64_t n_envs,
                       int n_sensors, tacsl_penalty_t params, int out_fp64, void* f_n, void* f_t, double* wrench,
-                      double* kin, uint8_t* contact, void* stream) {
+                      double* kin, uint8_t* contact, float* obs, void* stream) {
   if (!sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "force_field: null SDF");
   int rc = check_params(params);
   if (rc) return rc;
@@ -450,8 +459,10 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
   const int64_t frames = n_envs * n_sensors;
   if (frames == 0) return TACSL_OK;
   if (frames > 0x7fffffffLL) return set_error(TACSL_ERR_INVALID_ARGUMENT, "force_field: too many frames");
-  if (!taxels || !object_state || !sensor_state || !f_n || !f_t)
+  if (!taxels || !object_state || !sensor_state)
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "force_field: null pointer");
+  if (!f_n && !f_t && !wrench && !kin && !contact && !obs)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "force_field: no output buffer");
   const int n_taxels = rows * cols;
   const int threads = 128;
   Penalty P{params.k_n, params.k_d, params.k_t, params.mu};
@@ -459,11 +470,11 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
   if (out_fp64) {
     force_field_kernel<double><<<(unsigned)frames, threads, 0, s>>>(
         make_grid(sdf), taxels, n_taxels, object_state, object_stride, sensor_state, sensor_stride, n_sensors, P,
-        (double*)f_n, (double*)f_t, wrench, kin, contact);
+        (double*)f_n, (double*)f_t, wrench, kin, contact, obs);
   } else {
     force_field_kernel<float><<<(unsigned)frames, threads, 0, s>>>(
         make_grid(sdf), taxels, n_taxels, object_state, object_stride, sensor_state, sensor_stride, n_sensors, P,
-        (float*)f_n, (float*)f_t, wrench, kin, contact);
+        (float*)f_n, (float*)f_t, wrench, kin, contact, obs);
   }
   return check_launch("force_field_kernel");
 }

@@ -12,6 +12,11 @@ namespace tacsl {
 // operands directly.
 struct LutParams {
   float c[3][15];
+  // float-output epilogue (observation representation of
+  // envs/peg_tasks.py:453-458): 0 colour, 1 diff (rgb - nominal),
+  // 2 concat ([rgb, nominal], 6 channels)
+  int rep;
+  float nominal[3];
 };
 
 }  // namespace tacsl

@@ -238,7 +238,8 @@ __global__ void __launch_bounds__(kMaxThreads + 64, 1) rgb_bulk_kernel(const flo
       // np.gradient's one-sided border rows
       const float* p = in_buf + (size_t)s * in_stage + W + row_off;  // image row r0 + lr0
       uint32_t* op = reinterpret_cast<uint32_t*>(out_buf + (size_t)b * out_stage + row_off * 3);
-      float* of = F32 ? out_f32 + (((size_t)img * H + r0) * W + row_off) * 3 : nullptr;
+      const int och = L.rep == 2 ? 6 : 3;  // float channels per output pixel
+      float* of = F32 ? out_f32 + (((size_t)img * H + r0) * W + row_off) * och : nullptr;
       float4 c = *reinterpret_cast<const float4*>(p);
       float4 up = (r0 + lr0 > 0) ? *reinterpret_cast<const float4*>(p - W) : c;
 #pragma unroll
@@ -289,10 +290,24 @@ __global__ void __launch_bounds__(kMaxThreads + 64, 1) rgb_bulk_kernel(const flo
           }
           if (F32) {
             float4* o = reinterpret_cast<float4*>(of);
-            o[0] = make_float4(r01.x, g01.x, b01.x, r01.y);
-            o[1] = make_float4(g01.y, b01.y, r23.x, g23.x);
-            o[2] = make_float4(b23.x, r23.y, g23.y, b23.y);
-            of += (size_t)W * 3;
+            const float n0 = L.nominal[0], n1 = L.nominal[1], n2 = L.nominal[2];
+            if (L.rep == 0) {  // "color" (envs/peg_tasks.py:445, .astype(float32))
+              o[0] = make_float4(r01.x, g01.x, b01.x, r01.y);
+              o[1] = make_float4(g01.y, b01.y, r23.x, g23.x);
+              o[2] = make_float4(b23.x, r23.y, g23.y, b23.y);
+            } else if (L.rep == 1) {  // "diff": rgb - nominal (peg_tasks.py:453-454)
+              o[0] = make_float4(r01.x - n0, g01.x - n1, b01.x - n2, r01.y - n0);
+              o[1] = make_float4(g01.y - n1, b01.y - n2, r23.x - n0, g23.x - n1);
+              o[2] = make_float4(b23.x - n2, r23.y - n0, g23.y - n1, b23.y - n2);
+            } else {  // "concat": [rgb, nominal] on the channel axis (peg_tasks.py:455-458)
+              o[0] = make_float4(r01.x, g01.x, b01.x, n0);
+              o[1] = make_float4(n1, n2, r01.y, g01.y);
+              o[2] = make_float4(b01.y, n0, n1, n2);
+              o[3] = make_float4(r23.x, g23.x, b23.x, n0);
+              o[4] = make_float4(n1, n2, r23.y, g23.y);
+              o[5] = make_float4(b23.y, n0, n1, n2);
+            }
+            of += (size_t)W * och;
           }
         }
         up = c;
@@ -351,9 +366,20 @@ __global__ void __launch_bounds__(256) rgb_scalar_kernel(const float* __restrict
       out_u8[3 * p + 2] = (uint8_t)(q8(v2) & 0xFF);
     }
     if (out_f32) {
-      out_f32[3 * p + 0] = v0;
-      out_f32[3 * p + 1] = v1;
-      out_f32[3 * p + 2] = v2;
+      if (L.rep == 2) {
+        float* o = out_f32 + 6 * p;
+        o[0] = v0;
+        o[1] = v1;
+        o[2] = v2;
+        o[3] = L.nominal[0];
+        o[4] = L.nominal[1];
+        o[5] = L.nominal[2];
+      } else {
+        const bool diff = L.rep == 1;
+        out_f32[3 * p + 0] = diff ? v0 - L.nominal[0] : v0;
+        out_f32[3 * p + 1] = diff ? v1 - L.nominal[1] : v1;
+        out_f32[3 * p + 2] = diff ? v2 - L.nominal[2] : v2;
+      }
     }
   }
 }
@@ -475,6 +501,32 @@ extern "C" int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n
     case 2: return dispatch<2>(depth, n_images, height, width, rgb_u8, rgb_f32, lut->params, s);
     case 3: return dispatch<3>(depth, n_images, height, width, rgb_u8, rgb_f32, lut->params, s);
     case 4: return dispatch<4>(depth, n_images, height, width, rgb_u8, rgb_f32, lut->params, s);
+  }
+  return set_error(TACSL_ERR_INVALID_ARGUMENT, "LUT degree must be in [2, 4]");
+}
+
+extern "C" int tacsl_tactile_image_obs(tacsl_lut_t lut, const float* depth, int64_t n_images, int height, int width,
+                                       int rep, const float nominal[3], float* out, void* stream) {
+  if (!lut) return set_error(TACSL_ERR_INVALID_ARGUMENT, "tactile_image_obs: null LUT");
+  if (rep < 0 || rep > 2) return set_error(TACSL_ERR_INVALID_ARGUMENT, "tactile_image_obs: rep must be 0, 1 or 2");
+  if (width != lut->width || height != lut->height)
+    return set_error(TACSL_ERR_LUT_RESOLUTION_MISMATCH,
+                     "LUT calibrated at (" + std::to_string(lut->width) + ", " + std::to_string(lut->height) +
+                         "), image is (" + std::to_string(width) + ", " + std::to_string(height) + ")");
+  if (height < 2 || width < 2)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "tactile_image_obs: gradients need H >= 2 and W >= 2");
+  if (n_images < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "tactile_image_obs: negative image count");
+  if (n_images == 0) return TACSL_OK;
+  if (!depth || !out || (rep != 0 && !nominal))
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "tactile_image_obs: null pointer");
+  LutParams P = lut->params;
+  P.rep = rep;
+  for (int c = 0; c < 3; ++c) P.nominal[c] = rep ? nominal[c] : 0.f;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (lut->degree) {
+    case 2: return dispatch<2>(depth, n_images, height, width, nullptr, out, P, s);
+    case 3: return dispatch<3>(depth, n_images, height, width, nullptr, out, P, s);
+    case 4: return dispatch<4>(depth, n_images, height, width, nullptr, out, P, s);
   }
   return set_error(TACSL_ERR_INVALID_ARGUMENT, "LUT degree must be in [2, 4]");
 }

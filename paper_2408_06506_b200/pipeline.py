@@ -166,6 +166,41 @@ class SensorArray:
         return host
 
 
+class TactileObservations:
+    """Batched tactile observations of the 2-finger peg env: the outputs of
+    ``PegEnvBatch._tactile_images`` (envs/peg_tasks.py:434-459, without the
+    optional augmentation) and ``_tactile_ff`` (peg_tasks.py:461-477) for all
+    E envs x S sensors in two launches, with no per-sensor Python loop.
+
+    images: (E, S, H, W, 3) float32 ("color" / "diff") or (E, S, H, W, 6)
+    ("concat"); ff: (E, S, R, C, 3) float32 = [f_n.z, f_t.x, f_t.y] in each
+    sensor's frame.
+    """
+
+    def __init__(self, lut, sdf, points, params, n_envs, n_sensors=2, tactile_rep="color", device=None):
+        t = _device.torch()
+        self.device = _device.resolve_device(device)
+        self.lut = lut
+        self.sdf = device_sdf(sdf, self.device)
+        self.taxels = device_taxels(points, self.device)
+        self.rows, self.cols = int(points.rows), int(points.cols)
+        self.params = params
+        self.E, self.S = int(n_envs), int(n_sensors)
+        self.rep = tactile_rep
+        W, H = (int(v) for v in lut.image_size)
+        ch = 6 if tactile_rep == "concat" else 3
+        self.images = t.empty((self.E, self.S, H, W, ch), dtype=t.float32, device=self.device)
+        self.ff = t.empty((self.E, self.S, self.rows, self.cols, 3), dtype=t.float32, device=self.device)
+
+    def __call__(self, depth, obj_state, sen_state):
+        from .render import tactile_image_obs_device
+
+        tactile_image_obs_device(depth, self.lut, self.rep, out=self.images)
+        force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state, sen_state, self.params,
+                           obs=self.ff, n_sensors=self.S, obj_stride=13, sen_stride=13 * self.S, n_envs=self.E)
+        return self.images, self.ff
+
+
 def shard_range(n_envs: int, rank: int, world: int):
     """Contiguous env shard [lo, hi) of `rank`."""
     base, rem = divmod(n_envs, world)

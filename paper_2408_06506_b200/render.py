@@ -153,6 +153,33 @@ def depth_to_rgb_device(depth_values, lut, out_u8=None, out_f32=None, stream=Non
     return out_u8, out_f32
 
 
+_REPS = {"color": 0, "diff": 1, "concat": 2}
+
+
+def tactile_image_obs_device(depth_values, lut, rep="color", out=None, stream=None):
+    """Policy-observation image of envs/peg_tasks.py:434-458 (no augmentation):
+    (..., H, W) float32 CUDA depth -> (..., H, W, 3) float32 RGB ("color"),
+    RGB - nominal ("diff") or [RGB, nominal] (..., H, W, 6) ("concat"),
+    nominal = the LUT's background colour (peg_tasks.py:111-112)."""
+    t = _device.torch()
+    if rep not in _REPS:
+        raise ValueError(f"tactile_rep must be one of {sorted(_REPS)}")
+    dl = device_lut(lut)
+    v = depth_values
+    if not (_device.is_cuda_tensor(v) and v.dtype == t.float32 and v.is_contiguous()):
+        raise TypeError("tactile_image_obs_device wants a contiguous float32 CUDA tensor")
+    H, W = v.shape[-2], v.shape[-1]
+    ch = 6 if rep == "concat" else 3
+    if out is None:
+        out = t.empty(tuple(v.shape) + (ch,), dtype=t.float32, device=v.device)
+    n = int(np.prod(v.shape[:-2], dtype=np.int64)) if v.ndim > 2 else 1
+    nominal = np.ascontiguousarray(np.asarray(lut.coeffs, dtype=np.float64)[:, 0].astype(np.float32))
+    sh = _device.stream_handle(v.device) if stream is None else stream
+    _lib.check(_lib.load().tacsl_tactile_image_obs(dl.handle, v.data_ptr(), n, H, W, _REPS[rep],
+                                                   nominal.ctypes.data, out.data_ptr(), sh))
+    return out
+
+
 def depth_to_rgb(depth, lut, out_dtype=None):
     """Drop-in for gelsim.render.depth_to_rgb (render/lut.py:68-76).
 

@@ -131,27 +131,30 @@ def _state_array(pos, quat, v, w, E, name):
     return np.ascontiguousarray(np.concatenate(parts, axis=1))
 
 
-def force_field_device(sdf, taxels, rows, cols, obj_state, sen_state, params, f_n, f_t,
+def force_field_device(sdf, taxels, rows, cols, obj_state, sen_state, params, f_n=None, f_t=None,
                        wrench=None, kin=None, contact=None, n_sensors=1, obj_stride=13, sen_stride=None,
-                       stream=None):
+                       stream=None, obs=None, n_envs=None):
     """Device-level K2 on pre-allocated CUDA tensors.
 
     obj_state (E, 13) float64 (or one state with obj_stride=0); sen_state
-    (E, S, 13) float64; f_n, f_t (E, S, R, C, 3) float32 or float64.
+    (E, S, 13) float64; f_n, f_t (E, S, R, C, 3) float32 or float64; obs
+    (E, S, R, C, 3) float32 packed [f_n.z, f_t.x, f_t.y].  Any output may
+    be None (not all).
     """
     t = _device.torch()
-    dsdf = device_sdf(sdf, f_n.device)
-    n_frames = f_n.numel() // (rows * cols * 3)
-    E = n_frames // n_sensors
+    ref = next(x for x in (f_n, f_t, obs, wrench, kin, contact) if x is not None)
+    dsdf = device_sdf(sdf, ref.device)
+    if n_envs is None:
+        n_envs = sen_state.shape[0]
     if sen_stride is None:
         sen_stride = 13 * n_sensors
-    out64 = 1 if f_n.dtype == t.float64 else 0
+    out64 = 1 if (f_n is not None and f_n.dtype == t.float64) or (f_t is not None and f_t.dtype == t.float64) else 0
     lib = _lib.load()
-    sh = _device.stream_handle(f_n.device) if stream is None else stream
+    sh = _device.stream_handle(ref.device) if stream is None else stream
     _lib.check(lib.tacsl_force_field(
         dsdf.handle, taxels.data_ptr(), rows, cols, obj_state.data_ptr(), obj_stride, sen_state.data_ptr(),
-        sen_stride, E, n_sensors, _lib.penalty(params), out64, f_n.data_ptr(), f_t.data_ptr(),
-        _device.ptr(wrench), _device.ptr(kin), _device.ptr(contact), sh))
+        sen_stride, int(n_envs), n_sensors, _lib.penalty(params), out64, _device.ptr(f_n), _device.ptr(f_t),
+        _device.ptr(wrench), _device.ptr(kin), _device.ptr(contact), _device.ptr(obs), sh))
 
 
 def compute_force_field(points, object_sdf, object_pos, object_quat, object_linvel, object_angvel,

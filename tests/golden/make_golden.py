@@ -196,6 +196,22 @@ def make_depth(grid):
     np.savez_compressed(HERE / "depth.npz", **out)
 
 
+def make_formats():
+    """Files written by the reference's own writers: LUT text
+    (render/lut.py:122-137) and TFF1 frames (tactile/io.py:13-23)."""
+    from gelsim.render import write_lut
+    from gelsim.tactile import ForceField, write_force_field_frames
+
+    lut = synthetic_lut((320, 240), degree=3, seed=4)
+    lut.sensor_id = "gelpad-A"
+    lut.calibrated_on = "2026-01-15"
+    lut.residual_rms = 0.00123
+    write_lut(lut, HERE / "ref.lut")
+    z = np.load(HERE / "ff.npz")
+    frames = [ForceField(f_n=z["f_n"][e], f_t=z["f_t"][e]) for e in (0, 1)]
+    write_force_field_frames(HERE / "ref.tff", frames)
+
+
 if __name__ == "__main__":
     make_rgb()
     g = peg_grid_reference()
@@ -203,5 +219,6 @@ if __name__ == "__main__":
     make_ff(g)
     make_penalty()
     make_depth(g)
+    make_formats()
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)

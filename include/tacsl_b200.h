@@ -105,6 +105,38 @@ TACSL_API int tacsl_tactile_image_obs(tacsl_lut_t lut, const float* depth, int64
                                       int height, int width, int rep, const float nominal[3],
                                       float* out, void* stream);
 
+/* AugmentConfig (render/augment.py:15-48). */
+typedef struct {
+  double shift_px;
+  double zoom_lo, zoom_hi;
+  double brightness;
+  double contrast_lo, contrast_hi;
+  double saturation_lo, saturation_hi;
+  double hue;
+  int32_t channel_permutation;
+  double step_brightness;
+  double step_contrast_lo, step_contrast_hi;
+  double step_saturation_lo, step_saturation_hi;
+  double step_hue;
+  uint64_t seed;
+} tacsl_augment_cfg_t;
+
+/* Per-image augmentation parameters (augment.py:65-85) from the reference's
+ * tuple-keyed Philox streams, computed on the device: params (n, 16) float64
+ * = shift_x, shift_y, zoom, brightness, contrast, saturation, hue, perm[3],
+ * step brightness, contrast, saturation, hue. episode_seeds / step_indices
+ * are (n) int64 >= 0 device arrays. */
+TACSL_API int tacsl_augment_params(const tacsl_augment_cfg_t* cfg, const int64_t* episode_seeds,
+                                   const int64_t* step_indices, int64_t n, double* params,
+                                   void* stream);
+/* augment (augment.py:156-173) of float32 (n, H, W, 3) images with those
+ * parameters, then the observation representation rep 0 colour / 1 diff /
+ * 2 concat (envs/peg_tasks.py:453-458, nominal = HOST float[3]).  Out of
+ * place; out is (n, H, W, 3) or (n, H, W, 6) float32. */
+TACSL_API int tacsl_augment(const float* images, int64_t n, int height, int width,
+                            const double* params, int rep, const float nominal[3], float* out,
+                            void* stream);
+
 /* x (count) float32 -> u8 = clip(rint(255*x), 0, 255) (imageio.py:8-11). */
 TACSL_API int tacsl_to_uint8(const float* x, int64_t count, uint8_t* out, void* stream);
 

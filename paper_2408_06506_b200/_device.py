@@ -43,7 +43,8 @@ def to_device(x, dtype, device):
     t = torch()
     if isinstance(x, t.Tensor):
         return x.to(device=device, dtype=dtype).contiguous()
-    np_dtype = {t.float32: np.float32, t.float64: np.float64, t.uint8: np.uint8}[dtype]
+    np_dtype = {t.float32: np.float32, t.float64: np.float64, t.uint8: np.uint8, t.int64: np.int64,
+                t.int32: np.int32}[dtype]
     arr = np.ascontiguousarray(np.asarray(x, dtype=np_dtype))
     if not arr.flags.writeable:
         arr = arr.copy()

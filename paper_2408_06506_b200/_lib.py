@@ -22,6 +22,15 @@ class Penalty(ctypes.Structure):
     _fields_ = [("k_n", c_double), ("k_d", c_double), ("k_t", c_double), ("mu", c_double)]
 
 
+class AugmentCfg(ctypes.Structure):
+    _fields_ = [("shift_px", c_double), ("zoom_lo", c_double), ("zoom_hi", c_double), ("brightness", c_double),
+                ("contrast_lo", c_double), ("contrast_hi", c_double), ("saturation_lo", c_double),
+                ("saturation_hi", c_double), ("hue", c_double), ("channel_permutation", ctypes.c_int32),
+                ("step_brightness", c_double), ("step_contrast_lo", c_double), ("step_contrast_hi", c_double),
+                ("step_saturation_lo", c_double), ("step_saturation_hi", c_double), ("step_hue", c_double),
+                ("seed", ctypes.c_uint64)]
+
+
 # name -> (restype, argtypes); mirrors include/tacsl_b200.h one for one
 SIGNATURES = {
     "tacsl_abi_version": (c_int, []),
@@ -38,6 +47,8 @@ SIGNATURES = {
     "tacsl_force_field": (c_int, [c_void_p, P, c_int, c_int, P, c_int64, P, c_int64, c_int64, c_int,
                                   Penalty, c_int, P, P, P, P, P, P, c_void_p]),
     "tacsl_tactile_image_obs": (c_int, [c_void_p, P, c_int64, c_int, c_int, c_int, P, P, c_void_p]),
+    "tacsl_augment_params": (c_int, [ctypes.POINTER(AugmentCfg), P, P, c_int64, P, c_void_p]),
+    "tacsl_augment": (c_int, [P, c_int64, c_int, c_int, P, c_int, P, P, c_void_p]),
     "tacsl_net_wrench": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, c_void_p]),
     "tacsl_render_depth": (c_int, [c_void_p, P, P, c_int, c_int, P, c_double, c_double, c_double, c_int, P,
                                    c_int64, P, P, c_void_p]),

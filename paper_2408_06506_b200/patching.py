@@ -20,13 +20,14 @@ from __future__ import annotations
 import importlib
 
 _SITES = {
-    "gelsim.render": ("depth_to_rgb", "to_uint8", "render_depth"),
+    "gelsim.render": ("depth_to_rgb", "to_uint8", "render_depth", "augment"),
+    "gelsim.render.augment": ("augment",),
     "gelsim.render.lut": ("depth_to_rgb",),
     "gelsim.render.imageio": ("to_uint8",),
     "gelsim.render.depth": ("render_depth",),
     "gelsim.tactile": ("compute_force_field", "penalty_forces", "net_wrench"),
     "gelsim.tactile.field": ("compute_force_field", "penalty_forces", "net_wrench"),
-    "gelsim.envs.peg_tasks": ("depth_to_rgb", "compute_force_field", "render_depth"),
+    "gelsim.envs.peg_tasks": ("depth_to_rgb", "compute_force_field", "render_depth", "augment"),
     "gelsim.envs.scenes": ("depth_to_rgb", "compute_force_field", "render_depth"),
     "gelsim.envs.wrist": ("render_depth",),
     "gelsim.geometry": ("query_sdf",),
@@ -37,8 +38,10 @@ _saved: dict = {}
 
 def _impl(name):
     from . import depth, geometry, render, tactile
+    from .augment import augment as augment_fn
 
     return {
+        "augment": augment_fn,
         "render_depth": depth.render_depth,
         "depth_to_rgb": render.depth_to_rgb,
         "to_uint8": render.to_uint8,

@@ -177,8 +177,10 @@ class TactileObservations:
     sensor's frame.
     """
 
-    def __init__(self, lut, sdf, points, params, n_envs, n_sensors=2, tactile_rep="color", device=None):
+    def __init__(self, lut, sdf, points, params, n_envs, n_sensors=2, tactile_rep="color", device=None,
+                 augment=None):
         t = _device.torch()
+        self.augment_cfg = augment
         self.device = _device.resolve_device(device)
         self.lut = lut
         self.sdf = device_sdf(sdf, self.device)
@@ -192,10 +194,30 @@ class TactileObservations:
         self.images = t.empty((self.E, self.S, H, W, ch), dtype=t.float32, device=self.device)
         self.ff = t.empty((self.E, self.S, self.rows, self.cols, 3), dtype=t.float32, device=self.device)
 
-    def __call__(self, depth, obj_state, sen_state):
+        if augment is not None:
+            self._rgb = t.empty((self.E, self.S, H, W, 3), dtype=t.float32, device=self.device)
+            self._nominal = np.asarray(lut.coeffs, dtype=np.float64)[:, 0].astype(np.float32)
+
+    def __call__(self, depth, obj_state, sen_state, episode_seeds=None, step_indices=None):
+        """episode_seeds / step_indices: per-env int64 (the env's
+        int(env_seed * 1000003 + episode) and step_count, peg_tasks.py:449-450),
+        required when an AugmentConfig was given."""
         from .render import tactile_image_obs_device
 
-        tactile_image_obs_device(depth, self.lut, self.rep, out=self.images)
+        if self.augment_cfg is None:
+            tactile_image_obs_device(depth, self.lut, self.rep, out=self.images)
+        else:
+            from .augment import augment_device
+
+            t = _device.torch()
+            if episode_seeds is None or step_indices is None:
+                raise ValueError("augmentation needs per-env episode seeds and step indices")
+            tactile_image_obs_device(depth, self.lut, "color", out=self._rgb)
+            seeds = _device.to_device(episode_seeds, t.int64, self.device).reshape(self.E, 1)
+            steps = _device.to_device(step_indices, t.int64, self.device).reshape(self.E, 1)
+            augment_device(self._rgb, self.augment_cfg, seeds.expand(self.E, self.S).contiguous(),
+                           steps.expand(self.E, self.S).contiguous(), tactile_rep=self.rep,
+                           nominal=self._nominal, out=self.images)
         force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state, sen_state, self.params,
                            obs=self.ff, n_sensors=self.S, obj_stride=13, sen_stride=13 * self.S, n_envs=self.E)
         return self.images, self.ff

@@ -212,7 +212,44 @@ def make_formats():
     write_force_field_frames(HERE / "ref.tff", frames)
 
 
+AUG_CFGS = {
+    "full": dict(shift_px=2.5, zoom=(1.05, 1.2), brightness=0.1, contrast=(0.8, 1.2), saturation=(0.7, 1.3),
+                 hue=0.05, channel_permutation=True, step_brightness=0.02, step_contrast=(0.95, 1.05),
+                 step_saturation=(0.9, 1.1), step_hue=0.01, seed=3),
+    "color": dict(shift_px=0.0, zoom=(1.0, 1.0), brightness=0.2, contrast=(0.5, 1.5), saturation=(0.2, 1.8),
+                  hue=0.5, channel_permutation=False, step_brightness=0.0, step_contrast=(1.0, 1.0),
+                  step_saturation=(1.0, 1.0), step_hue=0.0, seed=11),
+    "spatial": dict(shift_px=6.0, zoom=(0.7, 1.4), brightness=0.0, contrast=(1.0, 1.0), saturation=(1.0, 1.0),
+                    hue=0.0, channel_permutation=True, step_brightness=0.0, step_contrast=(1.0, 1.0),
+                    step_saturation=(1.0, 1.0), step_hue=0.0, seed=0),
+    "identity": dict(shift_px=0.0, zoom=(1.0, 1.0), brightness=0.0, contrast=(1.0, 1.0), saturation=(1.0, 1.0),
+                     hue=0.0, channel_permutation=False, step_brightness=0.0, step_contrast=(1.0, 1.0),
+                     step_saturation=(1.0, 1.0), step_hue=0.0, seed=5),
+}
+AUG_SEEDS = [(0, 0), (17, 3), (2 ** 33 + 12345, 123), (987654321, 7)]
+
+
+def make_augment():
+    """render/augment.py:156-173 on float32 tactile images (the env applies
+    it to depth_to_rgb(...).astype(float32), envs/peg_tasks.py:445-452)."""
+    from gelsim.render import AugmentConfig, augment
+
+    out = {}
+    for size in ((80, 60), (40, 30)):
+        d, bg = depth_maps(size[0], size[1], len(AUG_SEEDS), config_id=106)
+        lut = scaled_lut(size, 2, seed=0, s=synthetic.lut_scale(size))
+        imgs = depth_to_rgb(DepthImage(values=d.astype(np.float64), background=bg), lut).astype(np.float32)
+        key = f"{size[1]}x{size[0]}"
+        out[f"img_{key}"] = imgs
+        for name, kw in AUG_CFGS.items():
+            cfg = AugmentConfig(**kw)
+            out[f"aug_{name}_{key}"] = np.stack([augment(imgs[i], cfg, ep, st)
+                                                 for i, (ep, st) in enumerate(AUG_SEEDS)])
+    np.savez_compressed(HERE / "augment.npz", **out)
+
+
 if __name__ == "__main__":
+    make_augment()
     make_rgb()
     g = peg_grid_reference()
     make_sdf(g)

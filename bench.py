@@ -229,7 +229,8 @@ def main():
     obj = torch.from_numpy(obj_all[lo:hi]).to(dev)
     sen = torch.from_numpy(np.ascontiguousarray(sen_all[lo:hi])).to(dev)
 
-    arr = SensorArray(lut, sdf, pts, params, E, S, device=dev, overlap=not args.no_overlap)
+    arr = SensorArray(lut, sdf, pts, params, E, S, device=dev, overlap=not args.no_overlap, rgb_u8=wl.rgb,
+                      with_ff=wl.ff)
     use_graph = not args.no_graph
     if use_graph:
         arr.capture(depth, obj, sen)
@@ -266,8 +267,8 @@ def main():
             torch.cuda.synchronize()
             return a.elapsed_time(b) / n
 
-        k1_ms = time_kernel(lambda: arr._launch_rgb(depth), args.steps)
-        k2_ms = time_kernel(lambda: arr._launch_ff(obj, sen), args.steps)
+        k1_ms = time_kernel(lambda: arr._launch_rgb(depth), args.steps) if wl.rgb else None
+        k2_ms = time_kernel(lambda: arr._launch_ff(obj, sen), args.steps) if wl.ff else None
     ms = max_over_ranks(ms_local)
     ms_per_step = ms / args.steps
     frames_total = wl.frames  # all ranks together
@@ -275,9 +276,9 @@ def main():
 
     # ---- end to end through the host-buffer API
     host = arr.host_buffers(pinned=True)
-    host["depth"].copy_(depth)
-    host["obj"].copy_(obj)
-    host["sen"].copy_(sen)
+    for k, v in (("depth", depth), ("obj", obj), ("sen", sen)):
+        if host[k] is not None:
+            host[k].copy_(v)
 
     def e2e_step():
         arr.run_host(host, depth, obj, sen, chunks=args.e2e_chunks)
@@ -294,23 +295,31 @@ def main():
     torch.cuda.synchronize()
     barrier()
     e2e_ms = max_over_ranks(a.elapsed_time(b)) / args.e2e_steps
-    h2d = sum(host[k].numel() * host[k].element_size() for k in ("depth", "obj", "sen")) * world
-    d2h = sum(host[k].numel() * host[k].element_size() for k in ("rgb", "f_n", "f_t", "wrench")) * world
+    h2d = sum(host[k].numel() * host[k].element_size() for k in ("depth", "obj", "sen")
+              if host[k] is not None) * world
+    d2h = sum(host[k].numel() * host[k].element_size() for k in ("rgb", "f_n", "f_t", "wrench")
+              if host[k] is not None) * world
 
     # ---- validation digest across ranks (outside every timed region)
     if world > 1:
         from paper_2408_06506_b200.pipeline import frame_checksum
-        dig = frame_checksum(arr.rgb_u8, arr.f_n, arr.f_t)
+        dig = frame_checksum(arr.rgb_u8, arr.f_n, arr.f_t)  # None-safe
         parts = [torch.zeros_like(dig) for _ in range(world)]
         dist.all_gather(parts, dig)
 
-    # ---- roofline of the dominant kernel (K1) and of the whole step
+    # ---- roofline of the dominant kernel (K1, or K2 when the step has no RGB) and of the whole step
     peak, peak_src = hbm_peak()
     bytes_ = arr.algorithmic_bytes()
-    k1_gbs = bytes_["rgb"] / (k1_ms / 1e3) / 1e9
     step_gbs = bytes_["total"] / (ms_local / args.steps / 1e3) / 1e9
-    key = f"rgb_bulk_kernel/config{wl.config_id}/world{world}"
-    traffic = traffic_from_profiles(key)
+    if wl.rgb:
+        kname, kms, kbytes = "rgb_bulk_kernel", k1_ms, bytes_["rgb"]
+        desc, rule = "rgb_bulk_kernel (K1 depth->RGB)", "7 B/px: 4 B fp32 depth read + 3 B uint8 RGB written"
+    else:
+        kname, kms, kbytes = "force_field_kernel", k2_ms, bytes_["ff"]
+        desc = "force_field_kernel (K2 force field + wrench; float64-ALU bound, HBM fraction shown)"
+        rule = "24 B/taxel fp32 f_n,f_t written + 208 B fp64 states read + 48 B wrench per frame"
+    k_gbs = kbytes / (kms / 1e3) / 1e9
+    traffic = traffic_from_profiles(f"{kname}/config{wl.config_id}/world{world}")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -322,13 +331,12 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                 "api": "SensorArray.run_host: pinned host depth+states in, pinned host RGB+forces+wrench out, "
                        f"{args.e2e_chunks} env chunks pipelined over H2D / kernels / D2H streams"},
-        "roofline": {"bound": "hbm", "kernel": "rgb_bulk_kernel (K1 depth->RGB)", "achieved": k1_gbs,
-                     "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak, "traffic": traffic,
-                     "peak_source": peak_src, "kernel_ms": k1_ms,
-                     "algorithmic_bytes_per_launch": bytes_["rgb"],
-                     "bytes_rule": "7 B/px: 4 B fp32 depth read + 3 B uint8 RGB written",
+        "roofline": {"bound": "hbm", "kernel": desc, "achieved": k_gbs,
+                     "peak": peak, "unit": "GB/s", "frac": k_gbs / peak, "traffic": traffic,
+                     "peak_source": peak_src, "kernel_ms": kms,
+                     "algorithmic_bytes_per_launch": kbytes, "bytes_rule": rule,
                      "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak,
-                     "k2_force_field_ms": k2_ms, "k2_bytes_per_launch": bytes_["ff"]},
+                     "k1_rgb_ms": k1_ms, "k2_force_field_ms": k2_ms, "k2_bytes_per_launch": bytes_["ff"]},
         "gpu_launches": arr.launches_per_step * args.steps,
         "clocks": clocks.summary(),
         "graph": use_graph, "overlap": not args.no_overlap,

@@ -18,7 +18,7 @@ import numpy as np
 _W = {}
 
 
-def _init(image_size, ff_grid, sdf_dims, degree, n_sensors, config_id, pool_maps):
+def _init(image_size, ff_grid, sdf_dims, degree, n_sensors, config_id, pool_maps, with_rgb=True, with_ff=True):
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
     from paper_2408_06506_b200 import synthetic
@@ -30,6 +30,7 @@ def _init(image_size, ff_grid, sdf_dims, degree, n_sensors, config_id, pool_maps
         lut=lut, pts=pts.points,
         sdf=(sdf.origin, sdf.spacing, sdf.dims, sdf.values, sdf.gradients),
         states=synthetic.peg_states(64, n_sensors, config_id=config_id),
+        with_rgb=with_rgb, with_ff=with_ff,
     )
 
 
@@ -47,9 +48,15 @@ def _run(args):
         d = depth[idx % len(depth)]
         objF = obj[(idx // S) % E]
         senF = sen.reshape(E * S, 13)[idx % (E * S)]
-        rgb, f_n, f_t, force, torque = O.sensor_frames(d, lut.coeffs, lut.degree, _W["pts"], _W["sdf"], objF,
-                                                       senF, (1000.0, 100.0, 10.0, 2.0))
-        acc += float(rgb[0, 0, 0, 0]) + float(force.sum())
+        if _W["with_rgb"]:
+            rgb = O.to_uint8(O.depth_to_rgb(d, lut.coeffs, lut.degree))
+            acc += float(rgb[0, 0, 0, 0])
+        if _W["with_ff"]:
+            f_n, f_t, _ = O.compute_force_field(_W["pts"], *_W["sdf"], objF[:, 0:3], objF[:, 3:7], objF[:, 7:10],
+                                                objF[:, 10:13], senF[:, 0:3], senF[:, 3:7], senF[:, 7:10],
+                                                senF[:, 10:13])
+            force, _ = O.net_wrench(f_n, f_t, _W["pts"])
+            acc += float(force.sum())
     return hi - lo, time.perf_counter() - t0, acc
 
 
@@ -60,7 +67,8 @@ class CpuBaseline:
         self.cores = int(cores or os.cpu_count() or 1)
         self.workload = workload
         init = (tuple(workload.image_size), tuple(workload.ff_grid), tuple(workload.sdf_dims),
-                workload.lut_degree, workload.n_sensors, workload.config_id, pool_maps)
+                workload.lut_degree, workload.n_sensors, workload.config_id, pool_maps,
+                getattr(workload, "rgb", True), getattr(workload, "ff", True))
         self.pool = ProcessPoolExecutor(max_workers=self.cores, initializer=_init, initargs=init)
         # warm every worker (imports + asset set-up) outside any timing
         list(self.pool.map(_run, [(i, i + 1) for i in range(self.cores)]))

@@ -20,7 +20,7 @@ from .tactile import device_taxels, force_field_device
 
 class SensorArray:
     def __init__(self, lut, sdf, points, params, n_envs, n_sensors=1, device=None, ff_fp64=False,
-                 rgb_u8=True, rgb_f32=False, overlap=True):
+                 rgb_u8=True, rgb_f32=False, overlap=True, with_ff=True):
         t = _device.torch()
         self.device = _device.resolve_device(device)
         self.lut = device_lut(lut)
@@ -36,10 +36,16 @@ class SensorArray:
         self.rgb_u8 = t.empty((self.E, self.S, H, W, 3), dtype=t.uint8, device=dev) if rgb_u8 else None
         self.rgb_f32 = t.empty((self.E, self.S, H, W, 3), dtype=t.float32, device=dev) if rgb_f32 else None
         ff_dtype = t.float64 if ff_fp64 else t.float32
-        self.f_n = t.empty((self.E, self.S, self.rows, self.cols, 3), dtype=ff_dtype, device=dev)
-        self.f_t = t.empty_like(self.f_n)
-        self.wrench = t.empty((self.E, self.S, 6), dtype=t.float64, device=dev)
-        self.overlap = overlap
+        self.with_rgb = rgb_u8 or rgb_f32
+        self.with_ff = with_ff
+        if with_ff:
+            self.f_n = t.empty((self.E, self.S, self.rows, self.cols, 3), dtype=ff_dtype, device=dev)
+            self.f_t = t.empty_like(self.f_n)
+            self.wrench = t.empty((self.E, self.S, 6), dtype=t.float64, device=dev)
+        else:
+            self.f_n = self.f_t = self.wrench = None
+        self.overlap = overlap and self.with_rgb and with_ff
+        self.launches_per_step = int(self.with_rgb) + int(with_ff)
         self._ff_stream = t.cuda.Stream(device=dev) if overlap else None
         self._graph = None
         self._graph_inputs = None
@@ -49,10 +55,12 @@ class SensorArray:
     def algorithmic_bytes(self) -> dict:
         px = self.H * self.W
         rgb_out = (3 if self.rgb_u8 is not None else 0) + (12 if self.rgb_f32 is not None else 0)
-        taxel_out = self.rows * self.cols * 3 * self.f_n.element_size() * 2
         F = self.E * self.S
-        rgb = F * px * (4 + rgb_out)
-        ff = F * (taxel_out + 13 * 8 + 6 * 8) + self.E * 13 * 8
+        rgb = F * px * (4 + rgb_out) if self.with_rgb else 0
+        ff = 0
+        if self.with_ff:
+            taxel_out = self.rows * self.cols * 3 * self.f_n.element_size() * 2
+            ff = F * (taxel_out + 13 * 8 + 6 * 8) + self.E * 13 * 8
         return {"rgb": rgb, "ff": ff, "total": rgb + ff}
 
     def launch(self, depth, obj_state, sen_state):
@@ -67,8 +75,10 @@ class SensorArray:
             self._launch_rgb(depth)
             main.wait_stream(self._ff_stream)
         else:
-            self._launch_rgb(depth)
-            self._launch_ff(obj_state, sen_state)
+            if self.with_rgb:
+                self._launch_rgb(depth)
+            if self.with_ff:
+                self._launch_ff(obj_state, sen_state)
 
     def _launch_rgb(self, depth):
         depth_to_rgb_device(depth, self.lut, out_u8=self.rgb_u8, out_f32=self.rgb_f32)
@@ -106,9 +116,6 @@ class SensorArray:
             self.launch(depth, obj_state, sen_state)
         return self.rgb_u8 if self.rgb_u8 is not None else self.rgb_f32, self.f_n, self.f_t, self.wrench
 
-    # kernels launched per step (for the bench's gpu_launches count)
-    launches_per_step = 2
-
     def host_buffers(self, pinned=True):
         """Pinned host mirrors of the step's inputs and outputs."""
         t = _device.torch()
@@ -117,14 +124,15 @@ class SensorArray:
             return t.empty(shape, dtype=dtype, pin_memory=pinned)
 
         W, H = self.W, self.H
+        ff = self.with_ff
         return {
-            "depth": like((self.E, self.S, H, W), t.float32),
-            "obj": like((self.E, 13), t.float64),
-            "sen": like((self.E, self.S, 13), t.float64),
+            "depth": like((self.E, self.S, H, W), t.float32) if self.with_rgb else None,
+            "obj": like((self.E, 13), t.float64) if ff else None,
+            "sen": like((self.E, self.S, 13), t.float64) if ff else None,
             "rgb": like(tuple(self.rgb_u8.shape), t.uint8) if self.rgb_u8 is not None else None,
-            "f_n": like(tuple(self.f_n.shape), self.f_n.dtype),
-            "f_t": like(tuple(self.f_t.shape), self.f_t.dtype),
-            "wrench": like(tuple(self.wrench.shape), t.float64),
+            "f_n": like(tuple(self.f_n.shape), self.f_n.dtype) if ff else None,
+            "f_t": like(tuple(self.f_t.shape), self.f_t.dtype) if ff else None,
+            "wrench": like(tuple(self.wrench.shape), t.float64) if ff else None,
         }
 
     def run_host(self, host, depth, obj_state, sen_state, chunks=8):
@@ -148,15 +156,21 @@ class SensorArray:
         outs = [("rgb", self.rgb_u8), ("f_n", self.f_n), ("f_t", self.f_t), ("wrench", self.wrench)]
         for lo, hi in bounds:
             with t.cuda.stream(self._h2d):
-                depth[lo:hi].copy_(host["depth"][lo:hi], non_blocking=True)
-                obj_state[lo:hi].copy_(host["obj"][lo:hi], non_blocking=True)
-                sen_state[lo:hi].copy_(host["sen"][lo:hi], non_blocking=True)
+                if self.with_rgb:
+                    depth[lo:hi].copy_(host["depth"][lo:hi], non_blocking=True)
+                if self.with_ff:
+                    obj_state[lo:hi].copy_(host["obj"][lo:hi], non_blocking=True)
+                    sen_state[lo:hi].copy_(host["sen"][lo:hi], non_blocking=True)
             main.wait_stream(self._h2d)
-            depth_to_rgb_device(depth[lo:hi], self.lut, out_u8=None if self.rgb_u8 is None else self.rgb_u8[lo:hi],
-                                out_f32=None if self.rgb_f32 is None else self.rgb_f32[lo:hi])
-            force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state[lo:hi], sen_state[lo:hi],
-                               self.params, self.f_n[lo:hi], self.f_t[lo:hi], wrench=self.wrench[lo:hi],
-                               n_sensors=self.S, obj_stride=13, sen_stride=13 * self.S)
+            if self.with_rgb:
+                depth_to_rgb_device(depth[lo:hi], self.lut,
+                                    out_u8=None if self.rgb_u8 is None else self.rgb_u8[lo:hi],
+                                    out_f32=None if self.rgb_f32 is None else self.rgb_f32[lo:hi])
+            if self.with_ff:
+                force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state[lo:hi],
+                                   sen_state[lo:hi], self.params, self.f_n[lo:hi], self.f_t[lo:hi],
+                                   wrench=self.wrench[lo:hi], n_sensors=self.S, obj_stride=13,
+                                   sen_stride=13 * self.S)
             self._d2h.wait_stream(main)
             with t.cuda.stream(self._d2h):
                 for name, dev_t in outs:
@@ -234,4 +248,7 @@ def frame_checksum(rgb_u8, f_n, f_t) -> np.ndarray:
     """Cheap per-shard digest for cross-rank validation: (sum of RGB bytes,
     sum |f_n|, sum |f_t|) as float64."""
     t = _device.torch()
-    return t.stack([rgb_u8.sum(dtype=t.float64), f_n.abs().sum(dtype=t.float64), f_t.abs().sum(dtype=t.float64)])
+    parts = [x.sum(dtype=t.float64) if x is not None and k == 0 else
+             (x.abs().sum(dtype=t.float64) if x is not None else t.zeros((), dtype=t.float64))
+             for k, x in enumerate((rgb_u8, f_n, f_t))]
+    return t.stack([p.to(parts[0].device) for p in parts])

@@ -33,6 +33,8 @@ class Workload:
     ff_grid: tuple         # (rows, cols)
     sdf_dims: tuple
     lut_degree: int = 2
+    rgb: bool = True          # tactile RGB in the step
+    ff: bool = True           # force field + wrench in the step
 
     @property
     def frames(self) -> int:
@@ -43,8 +45,8 @@ CONFIGS = {
     1: Workload(1, 1, 1, (320, 240), (20, 25), (32, 32, 64)),
     2: Workload(2, 1024, 2, (320, 240), (20, 25), (32, 32, 64)),
     3: Workload(3, 4096, 2, (320, 240), (20, 25), (32, 32, 64)),
-    4: Workload(4, 16384, 1, (320, 240), (80, 100), (128, 128, 128)),
-    5: Workload(5, 8192, 1, (640, 480), (20, 25), (32, 32, 64)),
+    4: Workload(4, 16384, 1, (320, 240), (80, 100), (128, 128, 128), rgb=False),
+    5: Workload(5, 8192, 1, (640, 480), (20, 25), (32, 32, 64), ff=False),
 }
 
 

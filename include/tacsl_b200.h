@@ -137,6 +137,15 @@ TACSL_API int tacsl_augment(const float* images, int64_t n, int height, int widt
                             const double* params, int rep, const float nominal[3], float* out,
                             void* stream);
 
+/* Separable filter with optional 2x decimation -- the north_star's Gaussian
+ * smoothing (step 1, Gaussian taps) and Gaussian-pyramid level (step 2,
+ * binomial [1,4,6,4,1]/16).  NOT in the reference:
+ *   out[y,x] = sum_ij taps[i] taps[j] in[clamp(s*y+i-R), clamp(s*x+j-R)]
+ * 'nearest' borders, 2R+1 <= 33 HOST float taps, out (n, ceil(H/s), ceil(W/s)). */
+TACSL_API int tacsl_separable_filter(const float* in, int64_t n_images, int height, int width,
+                                     const float* taps, int radius, int step, float* out,
+                                     void* stream);
+
 /* x (count) float32 -> u8 = clip(rint(255*x), 0, 255) (imageio.py:8-11). */
 TACSL_API int tacsl_to_uint8(const float* x, int64_t count, uint8_t* out, void* stream);
 

@@ -22,8 +22,10 @@
 // uint8 bytes are packed with PRMT.  HBM sees each depth byte read once and
 // each RGB byte written once (95% of the measured copy bandwidth at 240x320).
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "handles.h"
@@ -391,56 +393,75 @@ int env_int(const char* name, int dflt) {
   return v > 0 ? v : dflt;
 }
 
-// Row groups / rows per thread / ring depth.  Defaults keep ~100 KB of shared
-// memory per CTA (two CTAs per SM) with >= 2 bands per CTA in flight.
-Layout choose_layout(int H, int W, bool u8) {
-  const int QW = W / 4;
+// Rows per thread and ring depth (env-tunable); the number of row groups is
+// chosen per kernel instantiation and image size by launch_bulk.
+Layout base_layout(int H, int W, bool u8) {
+  (void)H;
+  (void)u8;
   Layout lay;
   lay.rpt = env_int("TACSL_RGB_RPT", kDefaultRpt) == 4 ? 4 : 8;
-  // Defaults measured on B200 at 240x320 (tools/sweep_rgb.py): 8 rows per
-  // thread, 3 row groups (24-row bands), a 2-deep input ring -> 113 KB of
-  // shared memory, two CTAs per SM.
-  const bool user_groups = std::getenv("TACSL_RGB_GROUPS") != nullptr;
-  int groups = env_int("TACSL_RGB_GROUPS", 3);
-  groups = std::max(1, std::min(groups, kMaxThreads / QW));
-  // no point in more groups than the image has rows
-  while (groups > 1 && (groups - 1) * lay.rpt >= H) --groups;
   lay.stages = std::max(1, std::min(env_int("TACSL_RGB_STAGES", 2), kMaxStages));
-  auto fill = [&]() {
-    lay.groups = groups;
-    lay.band = groups * lay.rpt;
-    lay.in_stage_floats = (size_t)(lay.band + 2) * W;
-    lay.out_stage_bytes = (size_t)lay.band * W * 3;
-  };
-  fill();
-  // shrink the band until two CTAs share an SM (default) or one CTA fits
-  const size_t target = user_groups ? kSmemPerSm : kSmemPerSm / 2;
-  while (groups > 1 && lay.bytes(u8) > target) {
-    --groups;
-    fill();
-  }
-  while (lay.stages > 1 && lay.bytes(u8) > kSmemPerSm) {
-    --lay.stages;
-  }
+  lay.groups = 1;
   return lay;
 }
 
+Layout with_groups(Layout lay, int groups, int W) {
+  lay.groups = groups;
+  lay.band = groups * lay.rpt;
+  lay.in_stage_floats = (size_t)(lay.band + 2) * W;
+  lay.out_stage_bytes = (size_t)lay.band * W * 3;
+  return lay;
+}
+
+int bulk_threads(int W, int groups) { return (((W / 4) * groups + 31) / 32) * 32 + 64; }  // + loader + storer
+
 template <int DEG, int RPT, bool U8, bool F32>
-int launch_bulk(const Layout& lay, const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32,
+int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32,
                 const LutParams& L, cudaStream_t stream) {
-  const int threads = (((W / 4) * lay.groups + 31) / 32) * 32 + 64;  // consumer warps + loader + storer
-  size_t smem = lay.bytes(U8);
   auto kern = rgb_bulk_kernel<DEG, RPT, U8, F32>;
   static std::mutex mu;
-  static size_t configured = 0;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    if (smem > configured) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return check_launch("rgb: cudaFuncSetAttribute");
-      configured = smem;
+  static bool configured = false;
+  static std::vector<std::array<int, 4>> cache;  // (H, W, stages) -> groups
+  const int QW = W / 4;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemPerSm) != cudaSuccess)
+      return check_launch("rgb: cudaFuncSetAttribute");
+    configured = true;
+  }
+  int groups = 0;
+  if (const char* g = std::getenv("TACSL_RGB_GROUPS")) {
+    groups = std::max(1, std::min(std::atoi(g), kMaxThreads / QW));
+    while (groups > 1 && with_groups(lay, groups, W).bytes(U8) > kSmemPerSm) --groups;
+    while (lay.stages > 1 && with_groups(lay, groups, W).bytes(U8) > kSmemPerSm) --lay.stages;
+  } else {
+    for (const auto& c : cache)
+      if (c[0] == H && c[1] == W && c[2] == lay.stages) groups = c[3];
+    if (!groups) {
+      // Most consumer threads resident per SM (measured to be what the
+      // shading throughput tracks -- tools/sweep_rgb.py); ties go to the
+      // taller band (less halo re-read).
+      long best = -1;
+      const int gmax = std::max(1, std::min(kMaxThreads / QW, (H + RPT - 1) / RPT));
+      for (int g = 1; g <= gmax; ++g) {
+        const Layout cand = with_groups(lay, g, W);
+        const size_t smem = cand.bytes(U8);
+        if (smem > kSmemPerSm) break;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bulk_threads(W, g), smem);
+        const long score = (long)per_sm * g * QW;
+        if (per_sm > 0 && score >= best) {
+          best = score;
+          groups = g;
+        }
+      }
+      if (!groups) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: band ring does not fit in shared memory");
+      cache.push_back({H, W, lay.stages, groups});
     }
   }
+  lay = with_groups(lay, groups, W);
+  const int threads = bulk_threads(W, groups);
+  const size_t smem = lay.bytes(U8);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm <= 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: band ring does not fit in shared memory");
@@ -462,7 +483,7 @@ int dispatch(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f3
                        ((reinterpret_cast<uintptr_t>(depth) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(f32) & 15) == 0) && ((reinterpret_cast<uintptr_t>(u8) & 3) == 0);
   if (aligned && !std::getenv("TACSL_RGB_FORCE_SCALAR")) {
-    const Layout lay = choose_layout(H, W, u8 != nullptr);
+    const Layout lay = base_layout(H, W, u8 != nullptr);
     if (lay.rpt == 4) {
       if (u8 && f32) return launch_bulk<DEG, 4, true, true>(lay, depth, n, H, W, u8, f32, L, stream);
       if (u8) return launch_bulk<DEG, 4, true, false>(lay, depth, n, H, W, u8, f32, L, stream);

@@ -68,7 +68,7 @@ __device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y
 struct Grid {
   const double4* __restrict__ cells;  // {d, gx, gy, gz} per cell, z fastest
   int nx, ny, nz;
-  double ox, oy, oz, spacing;
+  double ox, oy, oz, spacing, inv_spacing;
 };
 
 // 256-bit read-only load (LDG.E.ENL2.256 on sm_100): one trilinear corner
@@ -85,10 +85,21 @@ struct Cell {
   bool valid;
 };
 
+// Correctly rounded a / spacing in three DP operations: with y = RN(1/b)
+// (within half an ulp) and q = RN(a*y) (within one ulp), q + RN-corrected
+// by the exact FMA remainder is the correctly rounded quotient (Markstein's
+// theorem) -- bit-identical to numpy's true division, without __ddiv_rn's
+// reciprocal iteration.
+__device__ __forceinline__ double div_spacing(double a, const Grid& g) {
+  const double q = mul_rn(a, g.inv_spacing);
+  const double r = __fma_rn(-q, g.spacing, a);
+  return __fma_rn(r, g.inv_spacing, q);
+}
+
 __device__ __forceinline__ Cell locate(const Grid& g, V3 p) {
-  const double rx = __ddiv_rn(sub_rn(p.x, g.ox), g.spacing);
-  const double ry = __ddiv_rn(sub_rn(p.y, g.oy), g.spacing);
-  const double rz = __ddiv_rn(sub_rn(p.z, g.oz), g.spacing);
+  const double rx = div_spacing(sub_rn(p.x, g.ox), g);
+  const double ry = div_spacing(sub_rn(p.y, g.oy), g);
+  const double rz = div_spacing(sub_rn(p.z, g.oz), g);
   const double mx = (double)(g.nx - 1), my = (double)(g.ny - 1), mz = (double)(g.nz - 1);
   Cell c;
   c.valid = (rx >= 0.0) & (rx <= mx) & (ry >= 0.0) & (ry <= my) & (rz >= 0.0) & (rz <= mz);
@@ -400,6 +411,7 @@ Grid make_grid(tacsl_sdf_t sdf) {
   g.oy = sdf->origin[1];
   g.oz = sdf->origin[2];
   g.spacing = sdf->spacing;
+  g.inv_spacing = 1.0 / sdf->spacing;  // correctly rounded (IEEE division on the host)
   return g;
 }
 

@@ -26,11 +26,20 @@ struct RenderParams {
   int nx, ny, nz;
   double gox, goy, goz, spacing;
   double hix, hiy, hiz;  // origin + spacing * (dims - 1)  (depth.py:180-182)
+  double inv_spacing;    // RN(1 / spacing)
   double cx, cy, cz;     // camera position (sensor frame)
   double near_, far_, tol;
   int max_steps;
   int n_rays;
 };
+
+// correctly rounded a / spacing (Markstein: y = RN(1/b), q = RN(a y), one
+// exact-remainder correction), as in force_field.cu
+__device__ __forceinline__ double div_spacing(double a, const RenderParams& P) {
+  const double q = mul_rn(a, P.inv_spacing);
+  const double r = __fma_rn(-q, P.spacing, a);
+  return __fma_rn(r, P.inv_spacing, q);
+}
 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }  // np.maximum w/o NaNs
 __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
@@ -88,9 +97,9 @@ __global__ void __launch_bounds__(256) render_depth_kernel(const RenderParams P,
           const double bz = add_rn(dmax(sub_rn(P.goz, oz), 0.0), dmax(sub_rn(oz, P.hiz), 0.0));
           d = dmax(__dsqrt_rn(add_rn(add_rn(mul_rn(bx, bx), mul_rn(by, by)), mul_rn(bz, bz))), P.spacing);
         } else {
-          const double gx = __ddiv_rn(sub_rn(ox, P.gox), P.spacing);
-          const double gy = __ddiv_rn(sub_rn(oy, P.goy), P.spacing);
-          const double gz = __ddiv_rn(sub_rn(oz, P.goz), P.spacing);
+          const double gx = div_spacing(sub_rn(ox, P.gox), P);
+          const double gy = div_spacing(sub_rn(oy, P.goy), P);
+          const double gz = div_spacing(sub_rn(oz, P.goz), P);
           const int ix = min((int)gx, P.nx - 2), iy = min((int)gy, P.ny - 2), iz = min((int)gz, P.nz - 2);
           const double fx = sub_rn(gx, (double)ix), fy = sub_rn(gy, (double)iy), fz = sub_rn(gz, (double)iz);
           const double ux = sub_rn(1.0, fx), uy = sub_rn(1.0, fy), uz = sub_rn(1.0, fz);
@@ -143,6 +152,7 @@ extern "C" int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const dou
   P.goy = sdf->origin[1];
   P.goz = sdf->origin[2];
   P.spacing = sdf->spacing;
+  P.inv_spacing = 1.0 / sdf->spacing;
   P.hix = sdf->origin[0] + sdf->spacing * (double)(P.nx - 1);
   P.hiy = sdf->origin[1] + sdf->spacing * (double)(P.ny - 1);
   P.hiz = sdf->origin[2] + sdf->spacing * (double)(P.nz - 1);

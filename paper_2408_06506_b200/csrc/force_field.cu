@@ -25,12 +25,15 @@
 // the 32x32x64 peg, 64 MiB at 128^3).  Out of contact both forces are exactly
 // zero, so only contact taxels pay for the normal, velocities and penalty law.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "handles.h"
 
 namespace tacsl {
 namespace {
+
+constexpr int kFFMinBlocks = 4;  // resident CTAs per SM the register budget targets
 
 struct V3 {
   double x, y, z;
@@ -228,8 +231,8 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <typename OutT>
-__global__ void __launch_bounds__(128, 4) force_field_kernel(
+template <typename OutT, int MINB>
+__global__ void __launch_bounds__(128, MINB) force_field_kernel(
     const Grid grid, const double* __restrict__ taxels, int n_taxels, const double* __restrict__ obj_state,
     int64_t obj_stride, const double* __restrict__ sen_state, int64_t sen_stride, int n_sensors, const Penalty P,
     OutT* __restrict__ f_n_out, OutT* __restrict__ f_t_out, double* __restrict__ wrench, double* __restrict__ kin,
@@ -479,15 +482,22 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
   const int threads = 128;
   Penalty P{params.k_n, params.k_d, params.k_t, params.mu};
   cudaStream_t s = (cudaStream_t)stream;
-  if (out_fp64) {
-    force_field_kernel<double><<<(unsigned)frames, threads, 0, s>>>(
-        make_grid(sdf), taxels, n_taxels, object_state, object_stride, sensor_state, sensor_stride, n_sensors, P,
-        (double*)f_n, (double*)f_t, wrench, kin, contact, obs);
-  } else {
-    force_field_kernel<float><<<(unsigned)frames, threads, 0, s>>>(
-        make_grid(sdf), taxels, n_taxels, object_state, object_stride, sensor_state, sensor_stride, n_sensors, P,
-        (float*)f_n, (float*)f_t, wrench, kin, contact, obs);
-  }
+  const char* mb = std::getenv("TACSL_FF_MINBLOCKS");
+  const int minb = mb ? std::atoi(mb) : kFFMinBlocks;
+  auto launch = [&](auto* fn_tag, auto out_tag) {
+    using O = decltype(out_tag);
+    (void)fn_tag;
+    auto go = [&](auto kern) {
+      kern<<<(unsigned)frames, threads, 0, s>>>(make_grid(sdf), taxels, n_taxels, object_state, object_stride,
+                                              sensor_state, sensor_stride, n_sensors, P, (O*)f_n, (O*)f_t, wrench,
+                                              kin, contact, obs);
+    };
+    if (minb >= 6) go(force_field_kernel<O, 6>);
+    else if (minb == 5) go(force_field_kernel<O, 5>);
+    else go(force_field_kernel<O, 4>);
+  };
+  if (out_fp64) launch((int*)nullptr, double{});
+  else launch((int*)nullptr, float{});
   return check_launch("force_field_kernel");
 }
 

@@ -192,12 +192,21 @@ __global__ void augment_params_kernel(const tacsl_augment_cfg_t cfg, const int64
 __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ float clip01(float x) { return fminf(fmaxf(x, 0.f), 1.f); }
 
-// np.remainder(x, float32(1)): fmod, +1 for a negative remainder, +0 for zero
+// Correctly rounded a / b given y = RN(1/b): q = RN(a y) is within an ulp, and
+// one exact-remainder FMA correction rounds it correctly (Markstein) -- the
+// same bits as IEEE division, in 3 FP32 operations.
+__device__ __forceinline__ float div_y(float a, float b, float y) {
+  const float q = __fmul_rn(a, y);
+  const float r = __fmaf_rn(-q, b, a);
+  return __fmaf_rn(r, y, q);
+}
+
+// np.remainder(x, float32(1)): fmod (= x - trunc(x), exact for floats), +1 for
+// a negative remainder, +0 for zero
 __device__ __forceinline__ float rem1(float x) {
-  float m = fmodf(x, 1.0f);
+  float m = fsub(x, truncf(x));
   if (m < 0.f) m = fadd(m, 1.0f);
   return m == 0.f ? 0.f : m;
 }
@@ -217,11 +226,15 @@ __device__ __forceinline__ void apply_color(float v[3], double b, double c, doub
     const float r = clip01(v[0]), g = clip01(v[1]), bl = clip01(v[2]);
     const float mx = fmaxf(fmaxf(r, g), bl), mn = fminf(fminf(r, g), bl);
     const float span = fsub(mx, mn);
-    float sat = mx > 0.f ? fdiv(span, fmaxf(mx, 1e-12f)) : 0.f;
+    const float mxs = fmaxf(mx, 1e-12f);
+    float sat = mx > 0.f ? div_y(span, mxs, __frcp_rn(mxs)) : 0.f;
     const float safe = span > 0.f ? span : 1.f;
-    const float rc = fdiv(fsub(mx, r), safe), gc = fdiv(fsub(mx, g), safe), bc = fdiv(fsub(mx, bl), safe);
+    const float ys = __frcp_rn(safe);
+    const float rc = div_y(fsub(mx, r), safe, ys), gc = div_y(fsub(mx, g), safe, ys);
+    const float bc = div_y(fsub(mx, bl), safe, ys);
     float hue = (r == mx) ? fsub(bc, gc) : ((g == mx) ? fsub(fadd(2.f, rc), bc) : fsub(fadd(4.f, gc), rc));
-    hue = span > 0.f ? rem1(fdiv(hue, 6.f)) : 0.f;
+    constexpr float kInv6 = 0.16666667163372039794921875f;  // RN(1/6)
+    hue = span > 0.f ? rem1(div_y(hue, 6.f, kInv6)) : 0.f;
     // hue shift and saturation scale (augment.py:150-151)
     hue = rem1(fadd(hue, (float)h));
     sat = clip01(fmul(sat, (float)s));
@@ -262,8 +275,9 @@ __global__ void __launch_bounds__(256) augment_apply_kernel(const float* __restr
     if (zoom != 1.0 || sx != 0.0 || sy != 0.0) {
       // _resample_bilinear (augment.py:121-140)
       const float zf = (float)zoom;
-      float ys = fsub(fadd(fdiv(fsub((float)y, hc), zf), hc), (float)sy);
-      float xs = fsub(fadd(fdiv(fsub((float)x, wc), zf), wc), (float)sx);
+      const float izf = __frcp_rn(zf);
+      float ys = fsub(fadd(div_y(fsub((float)y, hc), zf, izf), hc), (float)sy);
+      float xs = fsub(fadd(div_y(fsub((float)x, wc), zf, izf), wc), (float)sx);
       ys = fminf(fmaxf(ys, 0.f), (float)(H - 1));
       xs = fminf(fmaxf(xs, 0.f), (float)(W - 1));
       const int y0 = min(max((int)ys, 0), H - 2), x0 = min(max((int)xs, 0), W - 2);

@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-overlap", action="store_true")
+    p.add_argument("--fused", action="store_true", help="one launch (force-field warps inside K1) per step")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--e2e-chunks", type=int, default=16, help="env chunks pipelined over H2D / compute / D2H")
@@ -230,7 +231,7 @@ def main():
     sen = torch.from_numpy(np.ascontiguousarray(sen_all[lo:hi])).to(dev)
 
     arr = SensorArray(lut, sdf, pts, params, E, S, device=dev, overlap=not args.no_overlap, rgb_u8=wl.rgb,
-                      with_ff=wl.ff)
+                      with_ff=wl.ff, fused=args.fused)
     use_graph = not args.no_graph
     if use_graph:
         arr.capture(depth, obj, sen)
@@ -269,6 +270,7 @@ def main():
 
         k1_ms = time_kernel(lambda: arr._launch_rgb(depth), args.steps) if wl.rgb else None
         k2_ms = time_kernel(lambda: arr._launch_ff(obj, sen), args.steps) if wl.ff else None
+        kf_ms = time_kernel(lambda: arr._launch_fused(depth, obj, sen), args.steps) if arr.fused else None
     ms = max_over_ranks(ms_local)
     ms_per_step = ms / args.steps
     frames_total = wl.frames  # all ranks together
@@ -311,7 +313,13 @@ def main():
     peak, peak_src = hbm_peak()
     bytes_ = arr.algorithmic_bytes()
     step_gbs = bytes_["total"] / (ms_local / args.steps / 1e3) / 1e9
-    if wl.rgb:
+    if arr.fused:
+        kname, kms, kbytes = "rgb_bulk_kernel_ff", kf_ms, bytes_["total"]
+        desc = ("rgb_bulk_kernel<..., FF> (fused step: K1 depth->RGB shading warps + K2 force-field warps "
+                "in one persistent launch)")
+        rule = ("7 B/px (4 B fp32 depth read + 3 B uint8 RGB written) + 24 B/taxel fp32 f_n,f_t + "
+                "208 B fp64 states + 48 B wrench per frame")
+    elif wl.rgb:
         kname, kms, kbytes = "rgb_bulk_kernel", k1_ms, bytes_["rgb"]
         desc, rule = "rgb_bulk_kernel (K1 depth->RGB)", "7 B/px: 4 B fp32 depth read + 3 B uint8 RGB written"
     else:
@@ -336,10 +344,12 @@ def main():
                      "peak_source": peak_src, "kernel_ms": kms,
                      "algorithmic_bytes_per_launch": kbytes, "bytes_rule": rule,
                      "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak,
-                     "k1_rgb_ms": k1_ms, "k2_force_field_ms": k2_ms, "k2_bytes_per_launch": bytes_["ff"]},
+                     "k1_rgb_ms": k1_ms, "k1_rgb_frac": (bytes_["rgb"] / (k1_ms / 1e3) / 1e9 / peak
+                                                         if k1_ms else None),
+                     "k2_force_field_ms": k2_ms, "k2_bytes_per_launch": bytes_["ff"], "fused_ms": kf_ms},
         "gpu_launches": arr.launches_per_step * args.steps,
         "clocks": clocks.summary(),
-        "graph": use_graph, "overlap": not args.no_overlap,
+        "graph": use_graph, "fused": arr.fused, "overlap": arr.overlap,
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

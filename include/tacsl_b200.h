@@ -219,6 +219,22 @@ TACSL_API int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows,
                       int out_fp64, void* f_n, void* f_t, double* wrench,
                       double* kin, uint8_t* contact, float* obs, void* stream);
 
+/* One sensor step in ONE launch: tacsl_depth_to_rgb (uint8) over n_images
+ * depth maps and tacsl_force_field (float32 f_n / f_t, float64 wrench) over
+ * n_envs x n_sensors frames, fused in one persistent kernel -- the force
+ * field runs in dedicated warps on the FP64 pipe beside the FP32 shading
+ * (the batched caller of envs/peg_tasks.py:434-477).  Same arguments and
+ * errors as the two calls; workspace = 8 bytes of device scratch (frame
+ * dispatch counter, zeroed by the call on `stream`).  Falls back to two
+ * launches when the image rows are not 16-byte aligned. */
+TACSL_API int tacsl_sensor_step(tacsl_lut_t lut, const float* depth, int64_t n_images, int height,
+                                int width, uint8_t* rgb_u8, tacsl_sdf_t sdf, const double* taxels,
+                                int rows, int cols, const double* object_state,
+                                int64_t object_stride, const double* sensor_state,
+                                int64_t sensor_stride, int64_t n_envs, int n_sensors,
+                                tacsl_penalty_t params, float* f_n, float* f_t, double* wrench,
+                                unsigned long long* workspace, void* stream);
+
 /* net_wrench on an existing field: f_n, f_t (frames, rows, cols, 3) float64,
  * points (rows, cols, 3) float64 -> force, torque (frames, 3) float64. */
 TACSL_API int tacsl_net_wrench(const double* f_n, const double* f_t, const double* points,

@@ -50,6 +50,8 @@ SIGNATURES = {
     "tacsl_augment_params": (c_int, [ctypes.POINTER(AugmentCfg), P, P, c_int64, P, c_void_p]),
     "tacsl_augment": (c_int, [P, c_int64, c_int, c_int, P, c_int, P, P, c_void_p]),
     "tacsl_separable_filter": (c_int, [P, c_int64, c_int, c_int, P, c_int, c_int, P, c_void_p]),
+    "tacsl_sensor_step": (c_int, [c_void_p, P, c_int64, c_int, c_int, P, c_void_p, P, c_int, c_int, P, c_int64, P,
+                                  c_int64, c_int64, c_int, Penalty, P, P, P, P, c_void_p]),
     "tacsl_net_wrench": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, c_void_p]),
     "tacsl_render_depth": (c_int, [c_void_p, P, P, c_int, c_int, P, c_double, c_double, c_double, c_int, P,
                                    c_int64, P, P, c_void_p]),

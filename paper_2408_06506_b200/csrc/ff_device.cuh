@@ -1,0 +1,369 @@
+// Device building blocks of K2 (penalty force field), shared by the
+// standalone force-field kernel (force_field.cu) and the fused sensor-step
+// kernel (rgb.cu).  See force_field.cu for the reference mapping.
+#pragma once
+
+#include "common.cuh"
+#include "handles.h"
+
+namespace tacsl {
+namespace {
+
+struct V3 {
+  double x, y, z;
+};
+
+__device__ __forceinline__ V3 v3(double x, double y, double z) { return V3{x, y, z}; }
+
+// ---- exact (numpy-order, no contraction) helpers --------------------------
+// np.cross: a1*b2 - a2*b1, a2*b0 - a0*b2, a0*b1 - a1*b0, each product rounded.
+__device__ __forceinline__ V3 cross_rn(V3 a, V3 b) {
+  return v3(sub_rn(mul_rn(a.y, b.z), mul_rn(a.z, b.y)), sub_rn(mul_rn(a.z, b.x), mul_rn(a.x, b.z)),
+            sub_rn(mul_rn(a.x, b.y), mul_rn(a.y, b.x)));
+}
+// transforms.py:36-43: (v + w*t) + qv x t with t = 2 (qv x v)
+__device__ __forceinline__ V3 quat_rotate_rn(double w, V3 qv, V3 v) {
+  V3 t = cross_rn(qv, v);
+  t = v3(2.0 * t.x, 2.0 * t.y, 2.0 * t.z);
+  const V3 c = cross_rn(qv, t);
+  return v3(add_rn(add_rn(v.x, mul_rn(w, t.x)), c.x), add_rn(add_rn(v.y, mul_rn(w, t.y)), c.y),
+            add_rn(add_rn(v.z, mul_rn(w, t.z)), c.z));
+}
+
+// ---- contracted helpers (off the mask chain) -------------------------------
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+  return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ V3 quat_rotate(double w, V3 qv, V3 v) {
+  V3 t = cross(qv, v);
+  t = v3(2.0 * t.x, 2.0 * t.y, 2.0 * t.z);
+  const V3 c = cross(qv, t);
+  return v3(v.x + w * t.x + c.x, v.y + w * t.y + c.y, v.z + w * t.z + c.z);
+}
+__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+
+struct Grid {
+  const double4* __restrict__ cells;  // {d, gx, gy, gz} per cell, z fastest
+  int nx, ny, nz;
+  double ox, oy, oz, spacing, inv_spacing;
+};
+
+// 256-bit read-only load (LDG.E.ENL2.256 on sm_100): one trilinear corner
+__device__ __forceinline__ double4 ldg256(const double4* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+// Cell location and trilinear weights of a query point (sdf.py:280-290)
+struct Cell {
+  size_t base;
+  double wx, wy, wz, ux, uy, uz;
+  bool valid;
+};
+
+// Correctly rounded a / spacing in three DP operations: with y = RN(1/b)
+// (within half an ulp) and q = RN(a*y) (within one ulp), q + RN-corrected
+// by the exact FMA remainder is the correctly rounded quotient (Markstein's
+// theorem) -- bit-identical to numpy's true division, without __ddiv_rn's
+// reciprocal iteration.
+__device__ __forceinline__ double div_spacing(double a, const Grid& g) {
+  const double q = mul_rn(a, g.inv_spacing);
+  const double r = __fma_rn(-q, g.spacing, a);
+  return __fma_rn(r, g.inv_spacing, q);
+}
+
+__device__ __forceinline__ Cell locate(const Grid& g, V3 p) {
+  const double rx = div_spacing(sub_rn(p.x, g.ox), g);
+  const double ry = div_spacing(sub_rn(p.y, g.oy), g);
+  const double rz = div_spacing(sub_rn(p.z, g.oz), g);
+  const double mx = (double)(g.nx - 1), my = (double)(g.ny - 1), mz = (double)(g.nz - 1);
+  Cell c;
+  c.valid = (rx >= 0.0) & (rx <= mx) & (ry >= 0.0) & (ry <= my) & (rz >= 0.0) & (rz <= mz);
+  // clip(rel, 0, dims - 1 - 1e-9); i0 = min(int(rel_c), dims - 2); f = rel_c - i0
+  const double cx = fmin(fmax(rx, 0.0), sub_rn(mx, 1e-9));
+  const double cy = fmin(fmax(ry, 0.0), sub_rn(my, 1e-9));
+  const double cz = fmin(fmax(rz, 0.0), sub_rn(mz, 1e-9));
+  const int ix = min((int)cx, g.nx - 2), iy = min((int)cy, g.ny - 2), iz = min((int)cz, g.nz - 2);
+  c.wx = sub_rn(cx, (double)ix);
+  c.wy = sub_rn(cy, (double)iy);
+  c.wz = sub_rn(cz, (double)iz);
+  c.ux = sub_rn(1.0, c.wx);
+  c.uy = sub_rn(1.0, c.wy);
+  c.uz = sub_rn(1.0, c.wz);
+  c.base = ((size_t)ix * g.ny + iy) * g.nz + iz;
+  return c;
+}
+
+// corner k = 4*dx + 2*dy + dz
+__device__ __forceinline__ size_t corner(const Grid& g, const Cell& c, int k) {
+  return c.base + (size_t)((k >> 2) & 1) * g.ny * g.nz + (size_t)((k >> 1) & 1) * g.nz + (k & 1);
+}
+
+// Trilinear distance, x then y then z lerps with every product and sum
+// rounded separately, as numpy evaluates sdf.py:305-311 -- bit-exact.
+__device__ __forceinline__ double interp_d(const Grid& g, const Cell& c) {
+  double v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __ldg(&g.cells[corner(g, c, k)].x);
+  const double d00 = add_rn(mul_rn(v[0], c.ux), mul_rn(v[4], c.wx));
+  const double d10 = add_rn(mul_rn(v[2], c.ux), mul_rn(v[6], c.wx));
+  const double d01 = add_rn(mul_rn(v[1], c.ux), mul_rn(v[5], c.wx));
+  const double d11 = add_rn(mul_rn(v[3], c.ux), mul_rn(v[7], c.wx));
+  const double d0 = add_rn(mul_rn(d00, c.uy), mul_rn(d10, c.wy));
+  const double d1 = add_rn(mul_rn(d01, c.uy), mul_rn(d11, c.wy));
+  return add_rn(mul_rn(d0, c.uz), mul_rn(d1, c.wz));
+}
+
+// Trilinear gradient, renormalised: n = g / max(|g|, 1e-12) (sdf.py:314-316)
+__device__ __forceinline__ V3 interp_n(const Grid& g, const Cell& c) {
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  double ax[2], ay[2], az[2];
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    double bx[2], by[2], bz[2];
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const double4 lo = ldg256(g.cells + corner(g, c, 2 * dy + dz));
+      const double4 hi = ldg256(g.cells + corner(g, c, 4 + 2 * dy + dz));
+      bx[dy] = lo.y * c.ux + hi.y * c.wx;
+      by[dy] = lo.z * c.ux + hi.z * c.wx;
+      bz[dy] = lo.w * c.ux + hi.w * c.wx;
+    }
+    ax[dz] = bx[0] * c.uy + bx[1] * c.wy;
+    ay[dz] = by[0] * c.uy + by[1] * c.wy;
+    az[dz] = bz[0] * c.uy + bz[1] * c.wy;
+  }
+  gx = ax[0] * c.uz + ax[1] * c.wz;
+  gy = ay[0] * c.uz + ay[1] * c.wz;
+  gz = az[0] * c.uz + az[1] * c.wz;
+  const double inv = rsqrt(fmax(gx * gx + gy * gy + gz * gz, 1e-24));
+  return v3(gx * inv, gy * inv, gz * inv);
+}
+
+struct Query {
+  double d;  // +inf when outside
+  V3 n;      // 0 when outside
+  bool valid;
+};
+
+// geometry/sdf.py:271-321
+__device__ __forceinline__ Query query(const Grid& g, V3 p) {
+  const Cell c = locate(g, p);
+  Query q;
+  q.valid = c.valid;
+  if (c.valid) {
+    q.d = interp_d(g, c);
+    q.n = interp_n(g, c);
+  } else {
+    q.d = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    q.n = v3(0.0, 0.0, 0.0);
+  }
+  return q;
+}
+
+struct Penalty {
+  double k_n, k_d, k_t, mu;
+};
+
+// tactile/field.py:61-76 on one point
+__device__ __forceinline__ void penalty(const Penalty& P, double d, double d_dot, V3 n, V3 vt, V3& fn, V3& ft,
+                                        bool& contact) {
+  contact = d < 0.0;
+  double coeff = contact ? (-P.k_n + P.k_d * d_dot) * d : 0.0;
+  coeff = fmax(coeff, 0.0);
+  fn = v3(coeff * n.x, coeff * n.y, coeff * n.z);
+  const double ss = vt.x * vt.x + vt.y * vt.y + vt.z * vt.z;
+  const double inv = rsqrt(ss);
+  const double speed = ss > 0.0 ? ss * inv : 0.0;
+  const bool slipping = contact && (speed > 1e-9);  // SLIP_VELOCITY_EPS, field.py:25
+  const double mag = fmin(P.k_t * speed, P.mu * coeff);
+  const double scale = slipping ? mag * inv : 0.0;
+  ft = v3(-scale * vt.x, -scale * vt.y, -scale * vt.z);
+}
+
+struct State {
+  V3 pos;
+  double qw;
+  V3 qv;
+  V3 v, w;
+};
+
+__device__ __forceinline__ State load_state(const double* __restrict__ s) {
+  State st;
+  st.pos = v3(__ldg(s + 0), __ldg(s + 1), __ldg(s + 2));
+  st.qw = __ldg(s + 3);
+  st.qv = v3(__ldg(s + 4), __ldg(s + 5), __ldg(s + 6));
+  st.v = v3(__ldg(s + 7), __ldg(s + 8), __ldg(s + 9));
+  st.w = v3(__ldg(s + 10), __ldg(s + 11), __ldg(s + 12));
+  return st;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Everything one force-field launch needs (kernel parameter).
+template <typename OutT>
+struct FFArgs {
+  Grid grid;
+  const double* __restrict__ taxels;
+  int n_taxels;
+  const double* __restrict__ obj_state;
+  int64_t obj_stride;
+  const double* __restrict__ sen_state;
+  int64_t sen_stride;
+  int n_sensors;
+  int64_t frames;
+  Penalty P;
+  OutT* __restrict__ f_n;
+  OutT* __restrict__ f_t;
+  double* __restrict__ wrench;
+  double* __restrict__ kin;
+  uint8_t* __restrict__ contact;
+  float* __restrict__ obs;
+  unsigned long long* counter;  // dynamic frame dispatch (fused step), zeroed before the launch
+};
+
+// Taxels first, first+stride, ... of one sensor frame (tactile/field.py:
+// 79-129); the wrench contributions (field.py:132-141) accumulate in acc.
+template <typename OutT>
+__device__ __forceinline__ void ff_frame(const FFArgs<OutT>& A, int64_t frame, int first, int stride,
+                                         double acc[6]) {
+  const int64_t e = frame / A.n_sensors;
+  const int s = (int)(frame - e * A.n_sensors);
+  const State O = load_state(A.obj_state + e * A.obj_stride);
+  const State S = load_state(A.sen_state + e * A.sen_stride + (int64_t)s * 13);
+  const V3 oq_inv = v3(-O.qv.x, -O.qv.y, -O.qv.z);
+  const V3 sq_inv = v3(-S.qv.x, -S.qv.y, -S.qv.z);
+  const bool want_kin = A.kin != nullptr;
+  const int64_t out_base = frame * (int64_t)A.n_taxels;
+  const Grid& grid = A.grid;
+  for (int i = first; i < A.n_taxels; i += stride) {
+    const double* tp = A.taxels + 3 * i;
+    const V3 p = v3(__ldg(tp), __ldg(tp + 1), __ldg(tp + 2));
+    // ---- mask chain, numpy order (field.py:104-107) ----
+    V3 pw = quat_rotate_rn(S.qw, S.qv, p);
+    pw = v3(add_rn(pw.x, S.pos.x), add_rn(pw.y, S.pos.y), add_rn(pw.z, S.pos.z));
+    const V3 ro = v3(sub_rn(pw.x, O.pos.x), sub_rn(pw.y, O.pos.y), sub_rn(pw.z, O.pos.z));
+    const V3 po = quat_rotate_rn(O.qw, oq_inv, ro);
+    const Cell cell = locate(grid, po);
+    const double d = cell.valid ? interp_d(grid, cell) : __longlong_as_double(0x7ff0000000000000LL);
+    const bool contact = d < 0.0;  // field.py:64
+    V3 fn = v3(0.0, 0.0, 0.0), ft = v3(0.0, 0.0, 0.0);
+    // Out of contact both forces are exactly zero (field.py:65-75), so the
+    // normal, the velocities and the penalty law run only for contact
+    // taxels -- unless the caller asked for the kinematics of every taxel.
+    if (contact || want_kin) {
+      const V3 n = cell.valid ? interp_n(grid, cell) : v3(0.0, 0.0, 0.0);
+      // ---- kinematics (field.py:109-115) ----
+      const V3 nw = quat_rotate(O.qw, O.qv, n);
+      const V3 rs = v3(pw.x - S.pos.x, pw.y - S.pos.y, pw.z - S.pos.z);
+      const V3 cs = cross(S.w, rs), co = cross(O.w, ro);
+      const V3 xd = v3((S.v.x + cs.x) - (O.v.x + co.x), (S.v.y + cs.y) - (O.v.y + co.y),
+                       (S.v.z + cs.z) - (O.v.z + co.z));
+      const double d_dot = dot(nw, xd);
+      const V3 vt = v3(xd.x - d_dot * nw.x, xd.y - d_dot * nw.y, xd.z - d_dot * nw.z);
+      if (contact) {
+        V3 fnw, ftw;
+        bool c2;
+        penalty(A.P, d, d_dot, nw, vt, fnw, ftw, c2);
+        // ---- back to the sensor frame (field.py:118-119) ----
+        fn = quat_rotate(S.qw, sq_inv, fnw);
+        ft = quat_rotate(S.qw, sq_inv, ftw);
+        // ---- net wrench (field.py:132-141) ----
+        const V3 f = v3(fn.x + ft.x, fn.y + ft.y, fn.z + ft.z);
+        const V3 tq = cross(p, f);
+        acc[0] += f.x;
+        acc[1] += f.y;
+        acc[2] += f.z;
+        acc[3] += tq.x;
+        acc[4] += tq.y;
+        acc[5] += tq.z;
+      }
+      if (want_kin) {
+        double* k = A.kin + (out_base + i) * 8;
+        k[0] = d;
+        k[1] = d_dot;
+        k[2] = vt.x;
+        k[3] = vt.y;
+        k[4] = vt.z;
+        k[5] = nw.x;
+        k[6] = nw.y;
+        k[7] = nw.z;
+      }
+    }
+    const int64_t o = (out_base + i) * 3;
+    if (A.f_n) {
+      A.f_n[o + 0] = (OutT)fn.x;
+      A.f_n[o + 1] = (OutT)fn.y;
+      A.f_n[o + 2] = (OutT)fn.z;
+    }
+    if (A.f_t) {
+      A.f_t[o + 0] = (OutT)ft.x;
+      A.f_t[o + 1] = (OutT)ft.y;
+      A.f_t[o + 2] = (OutT)ft.z;
+    }
+    if (A.obs) {  // policy observation [f_n.z, f_t.x, f_t.y] (envs/peg_tasks.py:474-476)
+      A.obs[o + 0] = (float)fn.z;
+      A.obs[o + 1] = (float)ft.x;
+      A.obs[o + 2] = (float)ft.y;
+    }
+    if (A.contact) A.contact[out_base + i] = contact ? 1 : 0;
+  }
+}
+
+// One warp computes whole frames (lane-strided taxels, shuffle-reduced
+// wrench): no CTA barrier, so these warps can run beside other work.
+template <typename OutT>
+__device__ __forceinline__ void ff_frames_warp(const FFArgs<OutT>& A, int64_t first_frame, int64_t frame_stride,
+                                               int lane) {
+  for (int64_t f = first_frame; f < A.frames; f += frame_stride) {
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    ff_frame(A, f, lane, 32, acc);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) acc[k] = warp_sum(acc[k]);
+    if (A.wrench && lane == 0)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) A.wrench[f * 6 + k] = acc[k];
+  }
+}
+
+// Frames handed out one at a time through a global counter, so every warp
+// that runs out of other work (force-field warps from the start, shading
+// warps after their last band) helps finish the force field.
+template <typename OutT>
+__device__ __forceinline__ void ff_frames_dynamic(const FFArgs<OutT>& A, int lane) {
+  while (true) {
+    unsigned long long f = 0;
+    if (lane == 0) f = atomicAdd(A.counter, 1ull);
+    f = __shfl_sync(0xffffffffu, f, 0);
+    if ((int64_t)f >= A.frames) break;
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    ff_frame(A, (int64_t)f, lane, 32, acc);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) acc[k] = warp_sum(acc[k]);
+    if (A.wrench && lane == 0)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) A.wrench[(int64_t)f * 6 + k] = acc[k];
+  }
+}
+
+inline Grid make_grid(tacsl_sdf_t sdf) {
+  Grid g;
+  g.cells = sdf->grid;
+  g.nx = sdf->dims[0];
+  g.ny = sdf->dims[1];
+  g.nz = sdf->dims[2];
+  g.ox = sdf->origin[0];
+  g.oy = sdf->origin[1];
+  g.oz = sdf->origin[2];
+  g.spacing = sdf->spacing;
+  g.inv_spacing = 1.0 / sdf->spacing;  // correctly rounded (IEEE division on the host)
+  return g;
+}
+
+}  // namespace
+}  // namespace tacsl

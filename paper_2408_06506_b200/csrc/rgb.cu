@@ -28,15 +28,18 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ff_device.cuh"
 #include "handles.h"
 
 namespace tacsl {
 namespace {
 
-constexpr int kMaxThreads = 320;  // consumer threads; + 2 producer warps = 384, 2 CTAs/SM: <= 85 registers
+constexpr int kMaxThreads = 320;  // consumer threads per CTA (+ 2 producer warps); 2 CTAs/SM at 240x320
+constexpr int kMaxThreadsFF = 480;  // fused step: one CTA per SM with the force-field warps
 constexpr int kMaxStages = 6;
 constexpr size_t kSmemPerSm = 227 * 1024;  // opt-in dynamic shared memory per CTA on sm_100
-constexpr int kDefaultRpt = 8;  // rows per thread per band (rolling 3-row register window)
+constexpr int kDefaultRpt = 8;
+constexpr int kFFWarps = 4;     // force-field warps per CTA in the fused sensor step  // rows per thread per band (rolling 3-row register window)
 
 __host__ __device__ constexpr int term_index(int i, int j) { return (i + j) * (i + j + 1) / 2 + j; }
 
@@ -116,12 +119,12 @@ struct Layout {
 //   empty[s] : every consumer warp has its rows of stage s in registers
 //   ready[b] : every consumer warp wrote its part of output tile b
 //   ofree[b] : the bulk store of tile b has finished reading it
-template <int DEG, int RPT, bool U8, bool F32>
-__global__ void __launch_bounds__(kMaxThreads + 64, 1) rgb_bulk_kernel(const float* __restrict__ depth,
+template <int DEG, int RPT, bool U8, bool F32, bool FF>
+__global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMaxThreads + 64, 1) rgb_bulk_kernel(const float* __restrict__ depth,
                                                                     int64_t n_images, int H, int W, int groups,
                                                                     int stages, uint8_t* __restrict__ out_u8,
                                                                     float* __restrict__ out_f32, const LutParams L,
-                                                                    int bulk_store) {
+                                                                    int bulk_store, const FFArgs<float> F) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int QW = W >> 2;
   const int n_cons = QW * groups;
@@ -173,6 +176,13 @@ __global__ void __launch_bounds__(kMaxThreads + 64, 1) rgb_bulk_kernel(const flo
         bulk_g2s(dst, src, bytes, &full[s]);
       }
     }
+    return;
+  }
+  if (FF && warp >= cons_warps + 2) {
+    // ------------------------------------------------ force-field warps ---
+    // K2 on the FP64 pipe beside the FP32/ALU-bound shading: each of the
+    // CTA's kFFWarps warps takes whole sensor frames (no CTA barrier).
+    ff_frames_dynamic(F, lane);
     return;
   }
   if (warp == cons_warps + 1) {
@@ -336,6 +346,7 @@ __global__ void __launch_bounds__(kMaxThreads + 64, 1) rgb_bulk_kernel(const flo
       ++img;
     }
   }
+  if (FF) ff_frames_dynamic(F, lane);  // out of bands: help finish the force field
 }
 
 // Generic path (any W >= 2, any alignment): one thread per pixel, neighbours
@@ -413,16 +424,20 @@ Layout with_groups(Layout lay, int groups, int W) {
   return lay;
 }
 
-int bulk_threads(int W, int groups) { return (((W / 4) * groups + 31) / 32) * 32 + 64; }  // + loader + storer
+// consumer warps + loader + storer (+ force-field warps in the fused step)
+int bulk_threads(int W, int groups, bool ff) {
+  return (((W / 4) * groups + 31) / 32) * 32 + 64 + (ff ? kFFWarps * 32 : 0);
+}
 
-template <int DEG, int RPT, bool U8, bool F32>
+template <int DEG, int RPT, bool U8, bool F32, bool FF = false>
 int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32,
-                const LutParams& L, cudaStream_t stream) {
-  auto kern = rgb_bulk_kernel<DEG, RPT, U8, F32>;
+                const LutParams& L, cudaStream_t stream, const FFArgs<float>* ff = nullptr) {
+  auto kern = rgb_bulk_kernel<DEG, RPT, U8, F32, FF>;
   static std::mutex mu;
   static bool configured = false;
   static std::vector<std::array<int, 4>> cache;  // (H, W, stages) -> groups
   const int QW = W / 4;
+  constexpr int kMaxCons = FF ? kMaxThreadsFF : kMaxThreads;
   std::lock_guard<std::mutex> lock(mu);
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemPerSm) != cudaSuccess)
@@ -431,7 +446,7 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
   }
   int groups = 0;
   if (const char* g = std::getenv("TACSL_RGB_GROUPS")) {
-    groups = std::max(1, std::min(std::atoi(g), kMaxThreads / QW));
+    groups = std::max(1, std::min(std::atoi(g), kMaxCons / QW));
     while (groups > 1 && with_groups(lay, groups, W).bytes(U8) > kSmemPerSm) --groups;
     while (lay.stages > 1 && with_groups(lay, groups, W).bytes(U8) > kSmemPerSm) --lay.stages;
   } else {
@@ -442,15 +457,15 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
       // shading throughput tracks -- tools/sweep_rgb.py); ties go to the
       // taller band (less halo re-read).
       long best = -1;
-      const int gmax = std::max(1, std::min(kMaxThreads / QW, (H + RPT - 1) / RPT));
+      const int gmax = std::max(1, std::min(kMaxCons / QW, (H + RPT - 1) / RPT));
       for (int g = 1; g <= gmax; ++g) {
         const Layout cand = with_groups(lay, g, W);
         const size_t smem = cand.bytes(U8);
         if (smem > kSmemPerSm) break;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bulk_threads(W, g), smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bulk_threads(W, g, FF), smem);
         const long score = (long)per_sm * g * QW;
-        if (per_sm > 0 && score >= best) {
+        if (per_sm > 0 && score > best) {
           best = score;
           groups = g;
         }
@@ -460,7 +475,7 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
     }
   }
   lay = with_groups(lay, groups, W);
-  const int threads = bulk_threads(W, groups);
+  const int threads = bulk_threads(W, groups, FF);
   const size_t smem = lay.bytes(U8);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
@@ -471,8 +486,10 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
   int64_t grid = std::min<int64_t>(units, (int64_t)sm_count(current_device()) * per_sm);
   int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
   if (std::getenv("TACSL_RGB_DEBUG_COPY")) bulk_store |= 2;
+  FFArgs<float> F{};
+  if (FF) F = *ff;
   kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
-                                                  bulk_store);
+                                                  bulk_store, F);
   return check_launch("rgb_bulk_kernel");
 }
 
@@ -548,6 +565,65 @@ extern "C" int tacsl_tactile_image_obs(tacsl_lut_t lut, const float* depth, int6
     case 2: return dispatch<2>(depth, n_images, height, width, nullptr, out, P, s);
     case 3: return dispatch<3>(depth, n_images, height, width, nullptr, out, P, s);
     case 4: return dispatch<4>(depth, n_images, height, width, nullptr, out, P, s);
+  }
+  return set_error(TACSL_ERR_INVALID_ARGUMENT, "LUT degree must be in [2, 4]");
+}
+
+namespace tacsl {
+namespace {
+
+template <int DEG>
+int fused_step(const LutParams& L, const float* depth, int64_t n, int H, int W, uint8_t* u8,
+               const FFArgs<float>& F, cudaStream_t stream) {
+  const Layout lay = base_layout(H, W, true);
+  if (lay.rpt == 4) return launch_bulk<DEG, 4, true, false, true>(lay, depth, n, H, W, u8, nullptr, L, stream, &F);
+  return launch_bulk<DEG, 8, true, false, true>(lay, depth, n, H, W, u8, nullptr, L, stream, &F);
+}
+
+}  // namespace
+}  // namespace tacsl
+
+extern "C" int tacsl_sensor_step(tacsl_lut_t lut, const float* depth, int64_t n_images, int height, int width,
+                                 uint8_t* rgb_u8, tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
+                                 const double* object_state, int64_t object_stride, const double* sensor_state,
+                                 int64_t sensor_stride, int64_t n_envs, int n_sensors, tacsl_penalty_t params,
+                                 float* f_n, float* f_t, double* wrench, unsigned long long* workspace,
+                                 void* stream) {
+  if (!lut || !sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "sensor_step: null handle");
+  if (width != lut->width || height != lut->height)
+    return set_error(TACSL_ERR_LUT_RESOLUTION_MISMATCH,
+                     "LUT calibrated at (" + std::to_string(lut->width) + ", " + std::to_string(lut->height) +
+                         "), image is (" + std::to_string(width) + ", " + std::to_string(height) + ")");
+  if (height < 2 || width < 2) return set_error(TACSL_ERR_INVALID_ARGUMENT, "sensor_step: H, W must be >= 2");
+  if (params.k_n < 0 || params.k_d < 0 || params.k_t < 0 || params.mu < 0)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "penalty parameters must be non-negative");
+  if (rows <= 0 || cols <= 0 || n_sensors <= 0 || n_envs < 0 || n_images < 0 || object_stride < 0 ||
+      sensor_stride < 0)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "sensor_step: bad sizes");
+  if (!depth || !rgb_u8 || !taxels || !object_state || !sensor_state || !f_n || !f_t)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "sensor_step: null pointer");
+  const int64_t frames = n_envs * n_sensors;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool aligned = (width % 4 == 0) && (width / 4 <= kMaxThreads) &&
+                       ((reinterpret_cast<uintptr_t>(depth) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(rgb_u8) & 3) == 0);
+  if (!aligned || n_images == 0 || frames == 0 || std::getenv("TACSL_STEP_UNFUSED")) {
+    // two launches: the image path does not fit the fused pipeline
+    int rc = tacsl_depth_to_rgb(lut, depth, n_images, height, width, rgb_u8, nullptr, stream);
+    if (rc) return rc;
+    return tacsl_force_field(sdf, taxels, rows, cols, object_state, object_stride, sensor_state, sensor_stride,
+                             n_envs, n_sensors, params, 0, f_n, f_t, wrench, nullptr, nullptr, nullptr, stream);
+  }
+  const FFArgs<float> F{make_grid(sdf), taxels, rows * cols, object_state, object_stride, sensor_state,
+                        sensor_stride, n_sensors, frames, Penalty{params.k_n, params.k_d, params.k_t, params.mu},
+                        f_n, f_t, wrench, nullptr, nullptr, nullptr, workspace};
+  if (!workspace) return set_error(TACSL_ERR_INVALID_ARGUMENT, "sensor_step: null workspace");
+  if (cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), s) != cudaSuccess)
+    return check_launch("sensor_step: workspace reset");
+  switch (lut->degree) {
+    case 2: return fused_step<2>(lut->params, depth, n_images, height, width, rgb_u8, F, s);
+    case 3: return fused_step<3>(lut->params, depth, n_images, height, width, rgb_u8, F, s);
+    case 4: return fused_step<4>(lut->params, depth, n_images, height, width, rgb_u8, F, s);
   }
   return set_error(TACSL_ERR_INVALID_ARGUMENT, "LUT degree must be in [2, 4]");
 }

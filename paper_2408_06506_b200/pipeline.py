@@ -20,7 +20,7 @@ from .tactile import device_taxels, force_field_device
 
 class SensorArray:
     def __init__(self, lut, sdf, points, params, n_envs, n_sensors=1, device=None, ff_fp64=False,
-                 rgb_u8=True, rgb_f32=False, overlap=True, with_ff=True):
+                 rgb_u8=True, rgb_f32=False, overlap=True, with_ff=True, fused=False):
         t = _device.torch()
         self.device = _device.resolve_device(device)
         self.lut = device_lut(lut)
@@ -44,8 +44,12 @@ class SensorArray:
             self.wrench = t.empty((self.E, self.S, 6), dtype=t.float64, device=dev)
         else:
             self.f_n = self.f_t = self.wrench = None
-        self.overlap = overlap and self.with_rgb and with_ff
-        self.launches_per_step = int(self.with_rgb) + int(with_ff)
+        # one fused launch (force-field warps beside the shading warps) when
+        # the step is uint8 RGB + float32 force field
+        self.fused = bool(fused and rgb_u8 and not rgb_f32 and with_ff and not ff_fp64)
+        self.overlap = overlap and self.with_rgb and with_ff and not self.fused
+        self.launches_per_step = 1 if self.fused else int(self.with_rgb) + int(with_ff)
+        self._workspace = t.zeros(1, dtype=t.int64, device=dev) if self.fused else None
         self._ff_stream = t.cuda.Stream(device=dev) if overlap else None
         self._graph = None
         self._graph_inputs = None
@@ -68,7 +72,9 @@ class SensorArray:
         joins back before returning)."""
         t = _device.torch()
         main = t.cuda.current_stream(self.device)
-        if self.overlap:
+        if self.fused:
+            self._launch_fused(depth, obj_state, sen_state)
+        elif self.overlap:
             self._ff_stream.wait_stream(main)
             with t.cuda.stream(self._ff_stream):
                 self._launch_ff(obj_state, sen_state)
@@ -79,6 +85,19 @@ class SensorArray:
                 self._launch_rgb(depth)
             if self.with_ff:
                 self._launch_ff(obj_state, sen_state)
+
+    def _launch_fused(self, depth, obj_state, sen_state, lo=0, hi=None):
+        from . import _lib
+        hi = self.E if hi is None else hi
+        E = hi - lo
+        d = depth[lo:hi]
+        lib = _lib.load()
+        _lib.check(lib.tacsl_sensor_step(
+            self.lut.handle, d.data_ptr(), E * self.S, self.H, self.W, self.rgb_u8[lo:hi].data_ptr(),
+            self.sdf.handle, self.taxels.data_ptr(), self.rows, self.cols, obj_state[lo:hi].data_ptr(), 13,
+            sen_state[lo:hi].data_ptr(), 13 * self.S, E, self.S, _lib.penalty(self.params),
+            self.f_n[lo:hi].data_ptr(), self.f_t[lo:hi].data_ptr(), self.wrench[lo:hi].data_ptr(),
+            self._workspace.data_ptr(), _device.stream_handle(self.device)))
 
     def _launch_rgb(self, depth):
         depth_to_rgb_device(depth, self.lut, out_u8=self.rgb_u8, out_f32=self.rgb_f32)
@@ -162,11 +181,13 @@ class SensorArray:
                     obj_state[lo:hi].copy_(host["obj"][lo:hi], non_blocking=True)
                     sen_state[lo:hi].copy_(host["sen"][lo:hi], non_blocking=True)
             main.wait_stream(self._h2d)
-            if self.with_rgb:
+            if self.fused:
+                self._launch_fused(depth, obj_state, sen_state, lo, hi)
+            elif self.with_rgb:
                 depth_to_rgb_device(depth[lo:hi], self.lut,
                                     out_u8=None if self.rgb_u8 is None else self.rgb_u8[lo:hi],
                                     out_f32=None if self.rgb_f32 is None else self.rgb_f32[lo:hi])
-            if self.with_ff:
+            if self.with_ff and not self.fused:
                 force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state[lo:hi],
                                    sen_state[lo:hi], self.params, self.f_n[lo:hi], self.f_t[lo:hi],
                                    wrench=self.wrench[lo:hi], n_sensors=self.S, obj_stride=13,

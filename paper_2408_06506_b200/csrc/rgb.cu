@@ -531,8 +531,8 @@ extern "C" int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n
   if (height < 2 || width < 2)
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "depth_to_rgb: gradients need H >= 2 and W >= 2");
   if (n_images < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "depth_to_rgb: negative image count");
-  if (!rgb_u8 && !rgb_f32) return set_error(TACSL_ERR_INVALID_ARGUMENT, "depth_to_rgb: no output buffer");
   if (n_images == 0) return TACSL_OK;
+  if (!rgb_u8 && !rgb_f32) return set_error(TACSL_ERR_INVALID_ARGUMENT, "depth_to_rgb: no output buffer");
   if (!depth) return set_error(TACSL_ERR_INVALID_ARGUMENT, "depth_to_rgb: null depth");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (lut->degree) {

@@ -131,14 +131,28 @@ def traffic_from_profiles(kernel_key):
         return None
 
 
+def workload_text(wl):
+    parts = []
+    if wl.rgb:
+        img = f"{wl.image_size[1]}x{wl.image_size[0]} RGB (uint8)"
+        if wl.smooth_sigma > 0:
+            img = f"Gaussian-smoothed (sigma={wl.smooth_sigma:g} px) {img}"
+        if wl.pyramid_levels > 1:
+            img += f" as a {wl.pyramid_levels}-level pyramid"
+        parts.append(img)
+    if wl.ff:
+        parts.append(f"{wl.ff_grid[0]}x{wl.ff_grid[1]} force field + wrench, peg SDF "
+                     f"{'x'.join(map(str, wl.sdf_dims))}")
+    return f"config {wl.config_id}: {wl.n_envs} envs x {wl.n_sensors} sensors, " + " + ".join(parts)
+
+
 def workload_config(wl, world):
     return {
-        "workload": f"config {wl.config_id}: {wl.n_envs} envs x {wl.n_sensors} sensors, "
-                    f"{wl.image_size[1]}x{wl.image_size[0]} RGB (uint8) + {wl.ff_grid[0]}x{wl.ff_grid[1]} "
-                    f"force field + wrench, peg SDF {'x'.join(map(str, wl.sdf_dims))}",
+        "workload": workload_text(wl),
         "envs": wl.n_envs, "sensors_per_env": wl.n_sensors, "sensor_frames_per_step": wl.frames,
         "image": [wl.image_size[1], wl.image_size[0]], "taxels": list(wl.ff_grid),
         "sdf_dims": list(wl.sdf_dims), "lut_degree": wl.lut_degree,
+        "pyramid_levels": wl.pyramid_levels, "smooth_sigma": wl.smooth_sigma,
         "parallelism": f"env-sharded x{world} (no data-path collective)",
         "l2": "inputs (2.5 GB depth at config 3) exceed the 126 MB L2; no flush needed",
     }
@@ -231,7 +245,8 @@ def main():
     sen = torch.from_numpy(np.ascontiguousarray(sen_all[lo:hi])).to(dev)
 
     arr = SensorArray(lut, sdf, pts, params, E, S, device=dev, overlap=not args.no_overlap, rgb_u8=wl.rgb,
-                      with_ff=wl.ff, fused=args.fused)
+                      with_ff=wl.ff, fused=args.fused, pyramid_levels=wl.pyramid_levels,
+                      smooth_sigma=wl.smooth_sigma)
     use_graph = not args.no_graph
     if use_graph:
         arr.capture(depth, obj, sen)
@@ -299,8 +314,8 @@ def main():
     e2e_ms = max_over_ranks(a.elapsed_time(b)) / args.e2e_steps
     h2d = sum(host[k].numel() * host[k].element_size() for k in ("depth", "obj", "sen")
               if host[k] is not None) * world
-    d2h = sum(host[k].numel() * host[k].element_size() for k in ("rgb", "f_n", "f_t", "wrench")
-              if host[k] is not None) * world
+    d2h = sum(v.numel() * v.element_size() for k, v in host.items()
+              if v is not None and k not in ("depth", "obj", "sen")) * world
 
     # ---- validation digest across ranks (outside every timed region)
     if world > 1:
@@ -319,9 +334,15 @@ def main():
                 "in one persistent launch)")
         rule = ("7 B/px (4 B fp32 depth read + 3 B uint8 RGB written) + 24 B/taxel fp32 f_n,f_t + "
                 "208 B fp64 states + 48 B wrench per frame")
-    elif wl.rgb:
+    elif wl.rgb and arr.levels == 1 and arr.sigma == 0:
         kname, kms, kbytes = "rgb_bulk_kernel", k1_ms, bytes_["rgb"]
         desc, rule = "rgb_bulk_kernel (K1 depth->RGB)", "7 B/px: 4 B fp32 depth read + 3 B uint8 RGB written"
+    elif wl.rgb:
+        kname, kms, kbytes = "image_pipeline", k1_ms, bytes_["rgb"]
+        desc = ("image pipeline: sep_bulk_kernel smoothing + rgb_bulk_kernel, then per pyramid level "
+                "sep_bulk_kernel pyr_down + rgb_bulk_kernel (all launches of the RGB side)")
+        rule = ("smoothing 8 B/px + K1 7 B/px at level 0; per level l>=1: pyr_down 20 B per output px + "
+                "K1 7 B/px")
     else:
         kname, kms, kbytes = "force_field_kernel", k2_ms, bytes_["ff"]
         desc = "force_field_kernel (K2 force field + wrench; float64-ALU bound, HBM fraction shown)"

@@ -18,7 +18,8 @@ import numpy as np
 _W = {}
 
 
-def _init(image_size, ff_grid, sdf_dims, degree, n_sensors, config_id, pool_maps, with_rgb=True, with_ff=True):
+def _init(image_size, ff_grid, sdf_dims, degree, n_sensors, config_id, pool_maps, with_rgb=True, with_ff=True,
+          levels=1, sigma=0.0):
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
     from paper_2408_06506_b200 import synthetic
@@ -30,8 +31,13 @@ def _init(image_size, ff_grid, sdf_dims, degree, n_sensors, config_id, pool_maps
         lut=lut, pts=pts.points,
         sdf=(sdf.origin, sdf.spacing, sdf.dims, sdf.values, sdf.gradients),
         states=synthetic.peg_states(64, n_sensors, config_id=config_id),
-        with_rgb=with_rgb, with_ff=with_ff,
+        with_rgb=with_rgb, with_ff=with_ff, levels=levels, sigma=sigma,
     )
+    if levels > 1 or sigma > 0:
+        from paper_2408_06506_b200 import smoothing
+        _W["taps"] = smoothing.gaussian_taps(sigma) if sigma > 0 else None
+        _W["binomial"] = smoothing.BINOMIAL5
+        _W["level_luts"] = [smoothing.level_lut(lut, lvl) for lvl in range(levels)]
 
 
 def _run(args):
@@ -48,7 +54,15 @@ def _run(args):
         d = depth[idx % len(depth)]
         objF = obj[(idx // S) % E]
         senF = sen.reshape(E * S, 13)[idx % (E * S)]
-        if _W["with_rgb"]:
+        if _W["with_rgb"] and "level_luts" in _W:
+            from oracle.pyramid_oracle import separable_filter
+            x = separable_filter(d, _W["taps"], 1) if _W["taps"] is not None else d
+            for lvl, ll in enumerate(_W["level_luts"]):
+                if lvl:
+                    x = separable_filter(x, _W["binomial"], 2)
+                rgb = O.to_uint8(O.depth_to_rgb(x, ll.coeffs, ll.degree))
+                acc += float(rgb[0, 0, 0, 0])
+        elif _W["with_rgb"]:
             rgb = O.to_uint8(O.depth_to_rgb(d, lut.coeffs, lut.degree))
             acc += float(rgb[0, 0, 0, 0])
         if _W["with_ff"]:
@@ -68,7 +82,8 @@ class CpuBaseline:
         self.workload = workload
         init = (tuple(workload.image_size), tuple(workload.ff_grid), tuple(workload.sdf_dims),
                 workload.lut_degree, workload.n_sensors, workload.config_id, pool_maps,
-                getattr(workload, "rgb", True), getattr(workload, "ff", True))
+                getattr(workload, "rgb", True), getattr(workload, "ff", True),
+                getattr(workload, "pyramid_levels", 1), getattr(workload, "smooth_sigma", 0.0))
         self.pool = ProcessPoolExecutor(max_workers=self.cores, initializer=_init, initargs=init)
         # warm every worker (imports + asset set-up) outside any timing
         list(self.pool.map(_run, [(i, i + 1) for i in range(self.cores)]))

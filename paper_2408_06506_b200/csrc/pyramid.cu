@@ -11,12 +11,25 @@
 // 2R+1 taps (Gaussian: scipy's truncate rule; pyramid: the 5-tap binomial
 // [1, 4, 6, 4, 1] / 16) and output stride s (1: smoothing, 2: pyramid level).
 //
-// A CTA streams the input rows of a 32-output-row band through a cp.async
-// ring, blurs each horizontally (only at the output columns) into a
-// (2R+1)-row ring, and emits every output row as the vertical blend of ring
-// rows -- HBM sees each input byte once (+ the 2R halo rows per band, mostly
-// L2 hits) and each output byte once.
+// Fast path (sep_bulk_kernel; W, Wo multiples of 4, 16-B aligned, R <= 8):
+// the K1 pipeline.  Persistent CTAs walk work units = (image, band of B
+// output rows); a loader warp brings the band's S*(B-1)+2R+1 input rows in
+// with ONE bulk-async copy (rows are contiguous) into a mbarrier-completed
+// ring, and consumer thread (g, xq) owns 4 output columns x RPT output rows:
+// it filters each input row it needs horizontally from 16-B shared loads and
+// folds it straight into RPT vertical accumulators (packed FFMA2) -- no
+// intermediate row ring, no CTA barrier -- then writes its quads with 16-B
+// coalesced stores.  HBM sees each input and output byte once (halo rows of
+// neighbouring bands come from L2).
+// Generic path (sep_filter_kernel): any size, cp.async row ring.
+//
+// Both paths accumulate in the same order (taps ascending, horizontal then
+// vertical, fp32 FMA from 0), so they agree bit for bit.
 #include <algorithm>
+#include <array>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "handles.h"
@@ -167,6 +180,291 @@ int launch_filter(const float* in, int64_t n, int H, int W, int Ho, int Wo, int 
   return check_launch("sep_filter_kernel");
 }
 
+
+// ------------------------------------------------------------------------
+// sep_bulk_kernel: warp-specialised band pipeline (see the file header).
+//   full[s]  : the band's input rows landed in stage s (TMA transaction)
+//   empty[s] : every consumer warp is done reading stage s
+// Output quads go straight to global memory (one 16-B store per thread and
+// row: a warp writes 512 contiguous bytes), which leaves all of shared
+// memory to the input ring.
+constexpr int kFMaxCons = 512;   // consumer threads per CTA (+ the loader warp)
+constexpr int kFMaxStages = 4;
+constexpr size_t kFSmem = 227 * 1024;
+
+struct FLayout {
+  int rpt = 8, groups = 1, stages = 2;
+  int band(void) const { return groups * rpt; }
+  size_t in_stage(int R, int S, int W) const { return (size_t)(S * (band() - 1) + 2 * R + 1) * W; }
+  size_t bytes(int R, int S, int W) const { return 128 + stages * in_stage(R, S, W) * sizeof(float); }
+};
+
+template <int R, int S, int RPT>
+__global__ void __launch_bounds__(kFMaxCons + 32, 1)
+    sep_bulk_kernel(const float* __restrict__ in, int64_t n, int H, int W, int Ho, int Wo, int groups, int stages,
+                    const Taps T, float* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int K = 2 * R + 1;
+  constexpr int NJ = S * (RPT - 1) + K;  // input rows behind one thread's RPT output rows
+  constexpr int OFF = 4 * ((R + 3) / 4);  // left reach, rounded up to a float4
+  constexpr int SPAN = 4 * S + 2 * OFF;   // input columns behind 4 output columns
+  const int QW = Wo >> 2;
+  const int n_cons = QW * groups;
+  const int cons_warps = (n_cons + 31) >> 5;  // host: blockDim.x == 32 * cons_warps + 32
+  const int band = groups * RPT;
+  const int bands = (Ho + band - 1) / band;
+  const int64_t units = n * bands;
+  const size_t in_stage = (size_t)(S * (band - 1) + K) * W;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kFMaxStages;
+  float* in_buf = reinterpret_cast<float*>(smem + 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], cons_warps);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+
+  if (warp == cons_warps) {
+    // ---------------------------------------------------------- loader ---
+    if (lane == 0) {
+      int k = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % stages;
+        if (k >= stages) mbar_wait_parity_sleep(&empty[s], (uint32_t)(k / stages - 1) & 1u);
+        // stage row i holds input row S*y0 - R + i; rows outside the image
+        // are not loaded (readers clamp onto the edge row, 'nearest')
+        const int64_t img = u / bands;
+        const int y0 = (int)(u - img * bands) * band;
+        const int y1 = min(y0 + band, Ho);
+        const int top = S * y0 - R;
+        const int rs = max(top, 0);
+        const int re = min(S * (y1 - 1) + R, H - 1);
+        const uint32_t bytes = (uint32_t)(re - rs + 1) * (uint32_t)W * 4u;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(in_buf + (size_t)s * in_stage + (size_t)(rs - top) * W, in + ((size_t)img * H + rs) * (size_t)W,
+                 bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers ---
+  const bool is_cons = (int)threadIdx.x < n_cons;
+  const int xq = threadIdx.x % QW;
+  const int g = is_cons ? (int)threadIdx.x / QW : groups;
+  const int xo0 = xq << 2;
+  const int xi0 = S * xo0 - OFF;  // first input column this thread loads
+  const bool interior = xi0 >= 0 && xi0 + SPAN <= W;
+  const int lr0 = g * RPT;
+
+  const int64_t g_img = gridDim.x / bands;
+  const int g_band = (int)(gridDim.x - g_img * bands);
+  int64_t img = blockIdx.x / bands;
+  int bidx = (int)(blockIdx.x - img * bands);
+  int s = 0;
+  uint32_t full_phase = 0;
+  while (img < n) {
+    const int y0 = bidx * band;
+    const int nrows = min(band, Ho - y0);
+    mbar_wait_parity(&full[s], full_phase);
+    float2 acc[RPT][2];
+    const bool active = lr0 < nrows;
+    if (active) {
+      const int top = S * y0 - R;
+      const float* stage = in_buf + (size_t)s * in_stage;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+      const int rbase = S * (y0 + lr0) - R;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int ri = min(max(rbase + j, 0), H - 1);
+        const float* row = stage + (size_t)(ri - top) * W;
+        float v[SPAN];
+        if (interior) {
+#pragma unroll
+          for (int i = 0; i < SPAN / 4; ++i) {
+            const float4 f = *reinterpret_cast<const float4*>(row + xi0 + 4 * i);
+            v[4 * i] = f.x;
+            v[4 * i + 1] = f.y;
+            v[4 * i + 2] = f.z;
+            v[4 * i + 3] = f.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < SPAN; ++i) v[i] = row[min(max(xi0 + i, 0), W - 1)];
+        }
+        float h[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float a = 0.f;
+#pragma unroll
+          for (int t = 0; t < K; ++t) a = __fmaf_rn(T.w[t], v[OFF + S * q + t - R], a);
+          h[q] = a;
+        }
+        const float2 h01 = make_float2(h[0], h[1]), h23 = make_float2(h[2], h[3]);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int t = j - S * r;
+          if (t >= 0 && t < K) {
+            acc[r][0] = __ffma2_rn(h01, make_float2(T.w[t], T.w[t]), acc[r][0]);
+            acc[r][1] = __ffma2_rn(h23, make_float2(T.w[t], T.w[t]), acc[r][1]);
+          }
+        }
+      }
+    }
+    // the stage is no longer read by this warp: release it before the stores
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (active) {
+      float* o = out + ((size_t)img * Ho + y0 + lr0) * (size_t)Wo + xo0;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+        if (lr0 + r < nrows)
+          *reinterpret_cast<float4*>(o + (size_t)r * Wo) =
+              make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
+    }
+    if (++s == stages) {
+      s = 0;
+      full_phase ^= 1u;
+    }
+    img += g_img;
+    bidx += g_band;
+    if (bidx >= bands) {
+      bidx -= bands;
+      ++img;
+    }
+  }
+}
+
+int bulk_threads_f(int Wo, int groups) { return (((Wo / 4) * groups + 31) / 32) * 32 + 32; }
+
+// Layout search: most consumer threads resident per SM (as for K1), ties to
+// the taller band (less halo re-read); env TACSL_FILTER_RPT / _GROUPS pin it.
+template <int R, int S, int RPT>
+int launch_bulk_filter(const float* in, int64_t n, int H, int W, int Ho, int Wo, const Taps& T, float* out,
+                       cudaStream_t stream, FLayout lay) {
+  auto kern = sep_bulk_kernel<R, S, RPT>;
+  static std::mutex mu;
+  static bool configured = false;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem) != cudaSuccess)
+      return check_launch("filter: cudaFuncSetAttribute");
+    configured = true;
+  }
+  const size_t smem = lay.bytes(R, S, W);
+  const int threads = bulk_threads_f(Wo, lay.groups);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  const int bands = (Ho + lay.band() - 1) / lay.band();
+  const int64_t grid = std::min<int64_t>(n * bands, (int64_t)sm_count(current_device()) * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, threads, smem, stream>>>(in, n, H, W, Ho, Wo, lay.groups, lay.stages, T, out);
+  return check_launch("sep_bulk_kernel");
+}
+
+template <int R, int S, int RPT>
+long score_layout(FLayout lay, int H, int W, int Ho, int Wo) {
+  const size_t smem = lay.bytes(R, S, W);
+  if (smem > kFSmem) return -1;
+  int per_sm = 0;
+  cudaFuncSetAttribute(sep_bulk_kernel<R, S, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sep_bulk_kernel<R, S, RPT>,
+                                                bulk_threads_f(Wo, lay.groups), smem);
+  (void)H;
+  (void)Ho;
+  return (long)per_sm * lay.groups * (Wo / 4);
+}
+
+int env_int_f(const char* name, int dflt) {
+  const char* s = std::getenv(name);
+  if (!s || !*s) return dflt;
+  const int v = std::atoi(s);
+  return v > 0 ? v : dflt;
+}
+
+template <int R, int S>
+int dispatch_bulk(const float* in, int64_t n, int H, int W, int Ho, int Wo, const Taps& T, float* out,
+                  cudaStream_t stream) {
+  static std::mutex mu;
+  static std::vector<std::array<int, 6>> cache;  // (H, W) -> (rpt, groups, stages)
+  FLayout best;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    bool found = false;
+    for (const auto& c : cache)
+      if (c[0] == H && c[1] == W) {
+        best.rpt = c[3];
+        best.groups = c[4];
+        best.stages = c[5];
+        found = true;
+      }
+    if (!found) {
+      const int QW = Wo / 4;
+      const int want_rpt = env_int_f("TACSL_FILTER_RPT", 0);
+      const int want_groups = env_int_f("TACSL_FILTER_GROUPS", 0);
+      const int stages = std::min(env_int_f("TACSL_FILTER_STAGES", 2), kFMaxStages);
+      long best_score = -1;
+      for (int rpt : {8, 4}) {
+        if ((want_rpt && rpt != want_rpt) || (rpt == 8 && R > 4)) continue;  // RPT=8 spills beyond R=4
+        const int gmax = std::max(1, std::min(kFMaxCons / QW, (Ho + rpt - 1) / rpt));
+        for (int g = 1; g <= gmax; ++g) {
+          if (want_groups && g != want_groups) continue;
+          for (int st = stages; st >= 1; --st) {
+            FLayout cand;
+            cand.rpt = rpt;
+            cand.groups = g;
+            cand.stages = st;
+            long sc;
+            if constexpr (R <= 4) {
+              sc = rpt == 8 ? score_layout<R, S, 8>(cand, H, W, Ho, Wo) : score_layout<R, S, 4>(cand, H, W, Ho, Wo);
+            } else {
+              sc = score_layout<R, S, 4>(cand, H, W, Ho, Wo);
+            }
+            if (sc <= 0) continue;
+            // a single stage cannot overlap the next band's load with this
+            // one's filtering: only a last resort
+            if (st < 2) sc = 1;
+            // strictly better occupancy wins; on a tie the taller band
+            if (sc > best_score || (sc == best_score && cand.band() > best.band())) {
+              best_score = sc;
+              best = cand;
+            }
+            break;  // deepest ring that fits for this (rpt, groups)
+          }
+        }
+      }
+      if (best_score <= 0) return -1;  // caller falls back to the generic kernel
+      cache.push_back({H, W, 0, best.rpt, best.groups, best.stages});
+    }
+  }
+  if constexpr (R <= 4) {
+    if (best.rpt == 8) return launch_bulk_filter<R, S, 8>(in, n, H, W, Ho, Wo, T, out, stream, best);
+  }
+  return launch_bulk_filter<R, S, 4>(in, n, H, W, Ho, Wo, T, out, stream, best);
+}
+
+template <int S>
+int dispatch_radius(int R, const float* in, int64_t n, int H, int W, int Ho, int Wo, const Taps& T, float* out,
+                    cudaStream_t stream) {
+  switch (R) {
+    case 1: return dispatch_bulk<1, S>(in, n, H, W, Ho, Wo, T, out, stream);
+    case 2: return dispatch_bulk<2, S>(in, n, H, W, Ho, Wo, T, out, stream);
+    case 3: return dispatch_bulk<3, S>(in, n, H, W, Ho, Wo, T, out, stream);
+    case 4: return dispatch_bulk<4, S>(in, n, H, W, Ho, Wo, T, out, stream);
+    case 5: return dispatch_bulk<5, S>(in, n, H, W, Ho, Wo, T, out, stream);
+    case 6: return dispatch_bulk<6, S>(in, n, H, W, Ho, Wo, T, out, stream);
+    case 7: return dispatch_bulk<7, S>(in, n, H, W, Ho, Wo, T, out, stream);
+    case 8: return dispatch_bulk<8, S>(in, n, H, W, Ho, Wo, T, out, stream);
+  }
+  return -1;
+}
+
 }  // namespace
 }  // namespace tacsl
 
@@ -189,6 +487,14 @@ extern "C" int tacsl_separable_filter(const float* in, int64_t n_images, int hei
   const size_t smem = ((size_t)kAhead * width + (size_t)(2 * radius + 1) * Wo) * sizeof(float);
   if (smem > 227 * 1024) return set_error(TACSL_ERR_INVALID_ARGUMENT, "filter: image too wide");
   cudaStream_t s = (cudaStream_t)stream;
+  const bool bulk_ok = width % 4 == 0 && Wo % 4 == 0 && Wo / 4 <= kFMaxCons && radius >= 1 && radius <= 8 &&
+                       (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                       !std::getenv("TACSL_FILTER_GENERIC");
+  if (bulk_ok) {
+    const int rc = step == 1 ? dispatch_radius<1>(radius, in, n_images, height, width, Ho, Wo, T, out, s)
+                             : dispatch_radius<2>(radius, in, n_images, height, width, Ho, Wo, T, out, s);
+    if (rc >= 0) return rc;  // -1: no band layout fits shared memory
+  }
   switch ((Wo + kThreads - 1) / kThreads) {
     case 1: return launch_filter<1>(in, n_images, height, width, Ho, Wo, step, T, out, s);
     case 2: return launch_filter<2>(in, n_images, height, width, Ho, Wo, step, T, out, s);

@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _device
+from . import _device, smoothing
 from .geometry import device_sdf
 from .render import depth_to_rgb_device, device_lut
 from .tactile import device_taxels, force_field_device
@@ -20,7 +20,8 @@ from .tactile import device_taxels, force_field_device
 
 class SensorArray:
     def __init__(self, lut, sdf, points, params, n_envs, n_sensors=1, device=None, ff_fp64=False,
-                 rgb_u8=True, rgb_f32=False, overlap=True, with_ff=True, fused=False):
+                 rgb_u8=True, rgb_f32=False, overlap=True, with_ff=True, fused=False, pyramid_levels=1,
+                 smooth_sigma=0.0):
         t = _device.torch()
         self.device = _device.resolve_device(device)
         self.lut = device_lut(lut)
@@ -44,11 +45,30 @@ class SensorArray:
             self.wrench = t.empty((self.E, self.S, 6), dtype=t.float64, device=dev)
         else:
             self.f_n = self.f_t = self.wrench = None
+        # optional image pipeline around K1 (north_star stages without a
+        # reference counterpart, smoothing.py): Gaussian smoothing of the
+        # depth (K5), then pyramid levels l >= 1 = K5 pyr_down + K1 with the
+        # level's LUT, each into its own uint8 RGB buffer
+        self.levels = max(1, int(pyramid_levels)) if self.with_rgb else 1
+        self.sigma = float(smooth_sigma) if self.with_rgb else 0.0
+        self._smooth = (t.empty((self.E, self.S, H, W), dtype=t.float32, device=dev) if self.sigma > 0 else None)
+        self._taps = smoothing.gaussian_taps(self.sigma) if self.sigma > 0 else None
+        self.rgb_levels = [self.rgb_u8]
+        self._lvl_depth = [None]
+        self._lvl_luts = [self.lut]
+        h, w = H, W
+        for lvl in range(1, self.levels):
+            h, w = -(-h // 2), -(-w // 2)
+            self._lvl_depth.append(t.empty((self.E, self.S, h, w), dtype=t.float32, device=dev))
+            self.rgb_levels.append(t.empty((self.E, self.S, h, w, 3), dtype=t.uint8, device=dev))
+            self._lvl_luts.append(device_lut(smoothing.level_lut(lut, lvl)))
         # one fused launch (force-field warps beside the shading warps) when
         # the step is uint8 RGB + float32 force field
-        self.fused = bool(fused and rgb_u8 and not rgb_f32 and with_ff and not ff_fp64)
+        self.fused = bool(fused and rgb_u8 and not rgb_f32 and with_ff and not ff_fp64 and self.levels == 1
+                          and self.sigma == 0)
         self.overlap = overlap and self.with_rgb and with_ff and not self.fused
-        self.launches_per_step = 1 if self.fused else int(self.with_rgb) + int(with_ff)
+        rgb_launches = (1 + int(self.sigma > 0) + 2 * (self.levels - 1)) if self.with_rgb else 0
+        self.launches_per_step = 1 if self.fused else rgb_launches + int(with_ff)
         self._workspace = t.zeros(1, dtype=t.int64, device=dev) if self.fused else None
         self._ff_stream = t.cuda.Stream(device=dev) if overlap else None
         self._graph = None
@@ -61,6 +81,13 @@ class SensorArray:
         rgb_out = (3 if self.rgb_u8 is not None else 0) + (12 if self.rgb_f32 is not None else 0)
         F = self.E * self.S
         rgb = F * px * (4 + rgb_out) if self.with_rgb else 0
+        if self.with_rgb and self.sigma > 0:
+            rgb += F * px * 8  # smoothing: fp32 depth read + smoothed depth written
+        for d in self._lvl_depth[1:]:
+            h, w = d.shape[-2:]
+            # pyr_down reads the level above (4 px per output px) and writes fp32;
+            # K1 reads the level and writes uint8 RGB
+            rgb += F * h * w * (16 + 4) + F * h * w * 7
         ff = 0
         if self.with_ff:
             taxel_out = self.rows * self.cols * 3 * self.f_n.element_size() * 2
@@ -99,8 +126,17 @@ class SensorArray:
             self.f_n[lo:hi].data_ptr(), self.f_t[lo:hi].data_ptr(), self.wrench[lo:hi].data_ptr(),
             self._workspace.data_ptr(), _device.stream_handle(self.device)))
 
-    def _launch_rgb(self, depth):
-        depth_to_rgb_device(depth, self.lut, out_u8=self.rgb_u8, out_f32=self.rgb_f32)
+    def _launch_rgb(self, depth, lo=0, hi=None):
+        hi = self.E if hi is None else hi
+        sl = slice(lo, hi)
+        d = depth[sl]
+        if self._smooth is not None:
+            d = smoothing.separable_filter_device(d, self._taps, 1, out=self._smooth[sl])
+        depth_to_rgb_device(d, self.lut, out_u8=None if self.rgb_u8 is None else self.rgb_u8[sl],
+                            out_f32=None if self.rgb_f32 is None else self.rgb_f32[sl])
+        for lvl in range(1, self.levels):
+            d = smoothing.pyr_down_device(d, out=self._lvl_depth[lvl][sl])
+            depth_to_rgb_device(d, self._lvl_luts[lvl], out_u8=self.rgb_levels[lvl][sl])
 
     def _launch_ff(self, obj_state, sen_state):
         force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state, sen_state, self.params,
@@ -152,6 +188,7 @@ class SensorArray:
             "f_n": like(tuple(self.f_n.shape), self.f_n.dtype) if ff else None,
             "f_t": like(tuple(self.f_t.shape), self.f_t.dtype) if ff else None,
             "wrench": like(tuple(self.wrench.shape), t.float64) if ff else None,
+            **{f"rgb_l{lvl}": like(tuple(self.rgb_levels[lvl].shape), t.uint8) for lvl in range(1, self.levels)},
         }
 
     def run_host(self, host, depth, obj_state, sen_state, chunks=8):
@@ -173,6 +210,7 @@ class SensorArray:
         bounds = [shard_range(self.E, i, chunks) for i in range(chunks)]
         bounds = [(lo, hi) for lo, hi in bounds if hi > lo]
         outs = [("rgb", self.rgb_u8), ("f_n", self.f_n), ("f_t", self.f_t), ("wrench", self.wrench)]
+        outs += [(f"rgb_l{lvl}", self.rgb_levels[lvl]) for lvl in range(1, self.levels)]
         for lo, hi in bounds:
             with t.cuda.stream(self._h2d):
                 if self.with_rgb:
@@ -184,9 +222,7 @@ class SensorArray:
             if self.fused:
                 self._launch_fused(depth, obj_state, sen_state, lo, hi)
             elif self.with_rgb:
-                depth_to_rgb_device(depth[lo:hi], self.lut,
-                                    out_u8=None if self.rgb_u8 is None else self.rgb_u8[lo:hi],
-                                    out_f32=None if self.rgb_f32 is None else self.rgb_f32[lo:hi])
+                self._launch_rgb(depth, lo, hi)
             if self.with_ff and not self.fused:
                 force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state[lo:hi],
                                    sen_state[lo:hi], self.params, self.f_n[lo:hi], self.f_t[lo:hi],

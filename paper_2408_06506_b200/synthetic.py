@@ -35,6 +35,8 @@ class Workload:
     lut_degree: int = 2
     rgb: bool = True          # tactile RGB in the step
     ff: bool = True           # force field + wrench in the step
+    pyramid_levels: int = 1   # RGB levels per frame (level l at 2^-l resolution)
+    smooth_sigma: float = 0.0  # Gaussian smoothing of the depth before shading
 
     @property
     def frames(self) -> int:
@@ -46,7 +48,7 @@ CONFIGS = {
     2: Workload(2, 1024, 2, (320, 240), (20, 25), (32, 32, 64)),
     3: Workload(3, 4096, 2, (320, 240), (20, 25), (32, 32, 64)),
     4: Workload(4, 16384, 1, (320, 240), (80, 100), (128, 128, 128), rgb=False),
-    5: Workload(5, 8192, 1, (640, 480), (20, 25), (32, 32, 64), ff=False),
+    5: Workload(5, 8192, 1, (640, 480), (20, 25), (32, 32, 64), ff=False, pyramid_levels=3, smooth_sigma=1.0),
 }
 
 

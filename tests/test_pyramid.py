@@ -81,3 +81,56 @@ def test_gpu_rgb_pyramid_vs_restatement():
         assert got.shape == ref.shape
         diff = np.abs(got.astype(int) - ref.astype(int))
         assert diff.max() <= 1 and (diff > 0).mean() < 2e-2, (lvl, diff.max(), (diff > 0).mean())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("hw", [(240, 320), (480, 640), (29, 40), (31, 72), (6, 16)])
+@pytest.mark.parametrize("radius", [1, 2, 4, 7])
+@pytest.mark.parametrize("step", [1, 2])
+def test_gpu_bulk_filter_equals_generic_bit_exact(monkeypatch, hw, radius, step):
+    """The warp-specialised band pipeline and the generic row-ring kernel
+    accumulate in the same order: identical bits, every size and radius."""
+    import torch
+    H, W = hw
+    if step == 2 and (-(-W // 2)) % 4:
+        pytest.skip("bulk path needs Wo % 4 == 0")
+    rng = np.random.default_rng(radius * 10 + step)
+    d = torch.from_numpy(rng.uniform(0.02, 0.025, size=(5, H, W)).astype(np.float32)).cuda()
+    taps = rng.uniform(0.1, 1.0, size=2 * radius + 1)
+    taps /= taps.sum()
+    fast = smoothing.separable_filter_device(d, taps, step)
+    monkeypatch.setenv("TACSL_FILTER_GENERIC", "1")
+    slow = smoothing.separable_filter_device(d, taps, step)
+    torch.cuda.synchronize()
+    assert torch.equal(fast, slow)
+    ref = separable_filter(d.cpu().numpy(), taps.astype(np.float32), step)
+    np.testing.assert_allclose(fast.cpu().numpy(), ref, rtol=0, atol=2e-8)
+
+
+@pytest.mark.gpu
+def test_sensor_array_pyramid_step_and_host_path():
+    """SensorArray with smoothing + 3 pyramid levels (config 5's step) equals
+    rgb_pyramid_device bit for bit, through the graph and the host path."""
+    import torch
+    from paper_2408_06506_b200 import SensorArray
+    from paper_2408_06506_b200.tactile import PenaltyParams
+    _, cam, bg, lut, pts = synthetic.sensor_setup((640, 480))
+    E = 6
+    d = torch.from_numpy(synthetic.depth_batch(cam, bg, E, config_id=73)).cuda().view(E, 1, 480, 640)
+    arr = SensorArray(lut, synthetic.peg_grid(), pts, PenaltyParams(), E, 1, with_ff=False, pyramid_levels=3,
+                      smooth_sigma=1.0)
+    assert arr.launches_per_step == 6
+    ref = smoothing.rgb_pyramid_device(d, lut, levels=3, sigma=1.0)
+    arr.capture(d, None, None)
+    arr.replay()
+    torch.cuda.synchronize()
+    for lvl in range(3):
+        assert torch.equal(arr.rgb_levels[lvl], ref[lvl]), lvl
+    host = arr.host_buffers()
+    host["depth"].copy_(d.cpu())
+    d2 = torch.zeros_like(d)
+    arr.run_host(host, d2, None, None, chunks=4)
+    torch.cuda.synchronize()
+    assert torch.equal(host["rgb"], ref[0].cpu())
+    assert torch.equal(host["rgb_l1"], ref[1].cpu())
+    assert torch.equal(host["rgb_l2"], ref[2].cpu())

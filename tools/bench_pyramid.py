@@ -15,6 +15,8 @@ px = N * 480 * 640
 cases = (("gaussian sigma=1", lambda: smoothing.gaussian_blur_device(d, 1.0), 8 * px),
          ("pyr_down", lambda: smoothing.pyr_down_device(d), 5 * px),
          ("rgb pyramid 3 levels + sigma=1", lambda: smoothing.rgb_pyramid_device(d, lut, 3, 1.0), None))
+if len(sys.argv) > 2 and sys.argv[2] == "filters":
+    cases = cases[:2]
 for name, fn, nbytes in cases:
     fn()
     torch.cuda.synchronize()

@@ -272,20 +272,25 @@ def main():
         ms_local = t0.elapsed_time(t1)
 
         # ---- per-kernel durations, each on its own launching stream
-        def time_kernel(fn, n):
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
+        def time_kernel(fn, n, segments=5):
+            # median over `segments` back-to-back event-timed segments of n launches
             s = torch.cuda.current_stream(dev)
-            a.record(s)
-            for _ in range(n):
-                fn()
-            b.record(s)
-            torch.cuda.synchronize()
-            return a.elapsed_time(b) / n
+            per = []
+            for _ in range(segments):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                for _ in range(n):
+                    fn()
+                b.record(s)
+                torch.cuda.synchronize()
+                per.append(a.elapsed_time(b) / n)
+            return float(np.median(per))
 
-        k1_ms = time_kernel(lambda: arr._launch_rgb(depth), args.steps) if wl.rgb else None
-        k2_ms = time_kernel(lambda: arr._launch_ff(obj, sen), args.steps) if wl.ff else None
-        kf_ms = time_kernel(lambda: arr._launch_fused(depth, obj, sen), args.steps) if arr.fused else None
+        nk = max(4, args.steps // 5)
+        k1_ms = time_kernel(lambda: arr._launch_rgb(depth), nk) if wl.rgb else None
+        k2_ms = time_kernel(lambda: arr._launch_ff(obj, sen), nk) if wl.ff else None
+        kf_ms = time_kernel(lambda: arr._launch_fused(depth, obj, sen), nk) if arr.fused else None
     ms = max_over_ranks(ms_local)
     ms_per_step = ms / args.steps
     frames_total = wl.frames  # all ranks together

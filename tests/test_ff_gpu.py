@@ -255,3 +255,85 @@ def test_query_sdf_sentinel_and_device_tensors():
     assert np.isinf(q.distance[1]) and np.all(q.normal[1] == 0)
     qd = query_sdf(g, torch.from_numpy(pts).cuda())
     assert torch.equal(qd.distance.cpu(), torch.from_numpy(q.distance))
+
+
+@pytest.mark.parametrize("offset", [0.0, 100.0])
+def test_fast_mask_chain_equals_exact_chain(monkeypatch, offset):
+    """force_field_fast_kernel (affine cell coordinates + exact fallback near
+    every decision boundary) against the all-exact kernel and the oracle:
+    identical contact masks, forces within 1e-9 relative -- also with the
+    envs placed 100 m from the world origin."""
+    t = torch
+    sdf = synthetic.peg_grid((32, 32, 64))
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 20, 25)
+    E, S = 256, 2
+    obj, sen = synthetic.peg_states(E, S, config_id=23, random_sensor_pose=True)
+    shift = np.array([offset, -0.5 * offset, 0.2 * offset])
+    obj[:, 0:3] += shift
+    sen[:, :, 0:3] += shift
+    dev = t.device("cuda")
+    tax = tactile.device_taxels(pts, dev)
+    o = t.from_numpy(obj).to(dev)
+    s = t.from_numpy(np.ascontiguousarray(sen)).to(dev)
+
+    def run():
+        f_n = t.empty((E, S, 20, 25, 3), dtype=t.float64, device=dev)
+        f_t = t.empty_like(f_n)
+        w = t.empty((E, S, 6), dtype=t.float64, device=dev)
+        c = t.empty((E, S, 20, 25), dtype=t.uint8, device=dev)
+        tactile.force_field_device(sdf, tax, 20, 25, o, s, PenaltyParams(), f_n, f_t, wrench=w, contact=c,
+                                   n_sensors=S)
+        t.cuda.synchronize()
+        return [x.cpu().numpy() for x in (f_n, f_t, w, c)]
+
+    fast = run()
+    monkeypatch.setenv("TACSL_FF_EXACT", "1")
+    exact = run()
+    assert np.array_equal(fast[3], exact[3])
+    assert 0.05 < fast[3].mean() < 0.6
+    # the reference chain itself rounds positions at ulp(|pos|): 100 m away
+    # the two chains legitimately differ by ~1e-14 m in d
+    rtol = 1e-9 if offset == 0 else 1e-6
+    for a, b in zip(fast[:3], exact[:3]):
+        assert vec_close(a, b, rtol, atol=1e-12)[0]
+    objE = np.repeat(obj, S, axis=0)
+    senE = sen.reshape(E * S, 13)
+    rn, rt, rk = O.compute_force_field(pts.points, *sdf_tuple(sdf), objE[:, 0:3], objE[:, 3:7], objE[:, 7:10],
+                                       objE[:, 10:13], senE[:, 0:3], senE[:, 3:7], senE[:, 7:10], senE[:, 10:13])
+    assert np.array_equal(fast[3].reshape(E * S, 20, 25).astype(bool), rk["d"] < 0)
+    assert vec_close(fast[0].reshape(rn.shape), rn, FF_RTOL, atol=1e-9)[0]
+    assert vec_close(fast[1].reshape(rt.shape), rt, FF_RTOL, atol=1e-9)[0]
+
+
+def test_fast_chain_decides_boundary_taxels_exactly(monkeypatch):
+    """Taxels placed exactly on the contact surface (d = 0 in the grid) and
+    on the grid boundary go through the exact fallback: masks still match."""
+    t = torch
+    sdf = geometry.box_grid((0.1, 0.1, 0.02), dims=(48, 48, 24), padding=0.01)
+    pts = sensor_grid(12, 12)
+    E = 64
+    rng = np.random.default_rng(5)
+    obj = np.zeros((E, 13))
+    obj[:, 3] = 1.0
+    sen = np.zeros((E, 1, 13))
+    sen[:, 0, 3] = 1.0
+    # the pad plane at z = 0.01 touches the box top (d = 0) for half of the envs
+    sen[:, 0, 2] = np.where(np.arange(E) % 2 == 0, 0.01, rng.uniform(0.0095, 0.0105, E)) - float(pts.points[0, 0, 2])
+    sen[:, 0, 7:10] = rng.normal(0, 0.01, (E, 3))
+    dev = t.device("cuda")
+    tax = tactile.device_taxels(pts, dev)
+    o = t.from_numpy(obj).to(dev)
+    s = t.from_numpy(sen).to(dev)
+
+    def run():
+        c = t.empty((E, 1, 12, 12), dtype=t.uint8, device=dev)
+        f_n = t.empty((E, 1, 12, 12, 3), dtype=t.float64, device=dev)
+        tactile.force_field_device(sdf, tax, 12, 12, o, s, PenaltyParams(), f_n, None, contact=c, n_sensors=1)
+        t.cuda.synchronize()
+        return c.cpu().numpy(), f_n.cpu().numpy()
+
+    fast_c, fast_f = run()
+    monkeypatch.setenv("TACSL_FF_EXACT", "1")
+    exact_c, exact_f = run()
+    assert np.array_equal(fast_c, exact_c)
+    assert vec_close(fast_f, exact_f, 1e-9, atol=1e-15)[0]

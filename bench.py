@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--fused", action="store_true", help="one launch (force-field warps inside K1) per step")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
-    p.add_argument("--e2e-chunks", type=int, default=16, help="env chunks pipelined over H2D / compute / D2H")
+    p.add_argument("--e2e-chunks", type=int, default=64, help="env chunks pipelined over H2D / compute / D2H")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample length")
     return p.parse_args()
 

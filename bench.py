@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--fused", action="store_true", help="one launch (force-field warps inside K1) per step")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     p.add_argument("--e2e-chunks", type=int, default=64, help="env chunks pipelined over H2D / compute / D2H")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample length")
     return p.parse_args()
@@ -297,30 +298,37 @@ def main():
     value = frames_total / (ms_per_step / 1e3)
 
     # ---- end to end through the host-buffer API
-    host = arr.host_buffers(pinned=True)
-    for k, v in (("depth", depth), ("obj", obj), ("sen", sen)):
-        if host[k] is not None:
-            host[k].copy_(v)
+    def measure_e2e():
+        host = arr.host_buffers(pinned=True)
+        for k, v in (("depth", depth), ("obj", obj), ("sen", sen)):
+            if host[k] is not None:
+                host[k].copy_(v)
 
-    def e2e_step():
-        arr.run_host(host, depth, obj, sen, chunks=args.e2e_chunks)
+        def e2e_step():
+            arr.run_host(host, depth, obj, sen, chunks=args.e2e_chunks)
 
-    e2e_step()
-    torch.cuda.synchronize()
-    barrier()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(args.e2e_steps):
         e2e_step()
-    b.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    e2e_ms = max_over_ranks(a.elapsed_time(b)) / args.e2e_steps
-    h2d = sum(host[k].numel() * host[k].element_size() for k in ("depth", "obj", "sen")
-              if host[k] is not None) * world
-    d2h = sum(v.numel() * v.element_size() for k, v in host.items()
-              if v is not None and k not in ("depth", "obj", "sen")) * world
+        torch.cuda.synchronize()
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = max_over_ranks(a.elapsed_time(b)) / args.e2e_steps
+        h2d = sum(host[k].numel() * host[k].element_size() for k in ("depth", "obj", "sen")
+                  if host[k] is not None) * world
+        d2h = sum(v.numel() * v.element_size() for k, v in host.items()
+                  if v is not None and k not in ("depth", "obj", "sen")) * world
+        return {"value": frames_total / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
+                "api": "SensorArray.run_host: pinned host depth+states in, pinned host RGB+forces+wrench out, "
+                       f"{args.e2e_chunks} env chunks pipelined over H2D / kernels / D2H streams"}
+
+    e2e = None if args.no_e2e else measure_e2e()
 
     # ---- validation digest across ranks (outside every timed region)
     if world > 1:
@@ -349,8 +357,9 @@ def main():
         rule = ("smoothing 8 B/px + K1 7 B/px at level 0; per level l>=1: pyr_down 20 B per output px + "
                 "K1 7 B/px")
     else:
-        kname, kms, kbytes = "force_field_kernel", k2_ms, bytes_["ff"]
-        desc = "force_field_kernel (K2 force field + wrench; float64-ALU bound, HBM fraction shown)"
+        kname, kms, kbytes = "force_field_fast_kernel", k2_ms, bytes_["ff"]
+        desc = ("force_field_fast_kernel (K2 force field + wrench; float64 / L2-gather-latency bound, "
+                "HBM fraction shown)")
         rule = "24 B/taxel fp32 f_n,f_t written + 208 B fp64 states read + 48 B wrench per frame"
     k_gbs = kbytes / (kms / 1e3) / 1e9
     traffic = traffic_from_profiles(f"{kname}/config{wl.config_id}/world{world}")
@@ -361,10 +370,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f32 (RGB) / f64 (force field)",
         "data": "synthetic (analytic spherical-indenter depth maps, analytic peg SDF, random peg poses)",
         "config": workload_config(wl, world),
-        "e2e": {"value": frames_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-                "api": "SensorArray.run_host: pinned host depth+states in, pinned host RGB+forces+wrench out, "
-                       f"{args.e2e_chunks} env chunks pipelined over H2D / kernels / D2H streams"},
+        "e2e": e2e,
         "roofline": {"bound": "hbm", "kernel": desc, "achieved": k_gbs,
                      "peak": peak, "unit": "GB/s", "frac": k_gbs / peak, "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kms,

@@ -65,6 +65,7 @@ typedef enum {
 
 typedef struct tacsl_lut_s* tacsl_lut_t;
 typedef struct tacsl_sdf_s* tacsl_sdf_t;
+typedef struct tacsl_binned_lut_s* tacsl_binned_lut_t;
 
 /* PenaltyParams (tactile/field.py:28-37). */
 typedef struct {
@@ -94,6 +95,22 @@ TACSL_API void tacsl_lut_destroy(tacsl_lut_t lut);
 TACSL_API int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n_images,
                        int height, int width, uint8_t* rgb_u8, float* rgb_f32,
                        void* stream);
+
+/* Per-pixel BINNED polynomial LUT (north_star; NO reference counterpart --
+ * gelsim's PolyLut render/lut.py:31-59 is one global polynomial, which is
+ * the bins_y = bins_x = 1 case).  Pixel (y, x) uses coefficient set
+ * (y*bins_y/H, x*bins_x/W) (integer floor).  coeffs: HOST
+ * (bins_y, bins_x, 3, n_terms) float64 in monomial_exponents order; the
+ * table is uploaded to `device`.  INVALID_ARGUMENT for a degree outside
+ * [2,4], bins outside [1, image size] or a table larger than shared memory. */
+TACSL_API int tacsl_binned_lut_create(int device, const double* coeffs, int degree, int bins_y,
+                                      int bins_x, int width, int height, tacsl_binned_lut_t* out);
+TACSL_API void tacsl_binned_lut_destroy(tacsl_binned_lut_t lut);
+
+/* tacsl_depth_to_rgb through a binned LUT (same layouts, outputs and errors). */
+TACSL_API int tacsl_depth_to_rgb_binned(tacsl_binned_lut_t lut, const float* depth, int64_t n_images,
+                                        int height, int width, uint8_t* rgb_u8, float* rgb_f32,
+                                        void* stream);
 
 /* Policy observation image of envs/peg_tasks.py:434-458 without
  * augmentation: depth (N, H, W) -> float32 RGB in the env's representation,

@@ -15,6 +15,7 @@ fallback: without a B200 every compute call raises RuntimeError.
 """
 from . import formats
 from .augment import AugmentConfig, augment
+from .binned import BinnedPolyLut, depth_to_rgb_binned
 from .depth import render_depth
 from .errors import DimensionMismatch, GelsimError, InvalidQuery, LutResolutionMismatch
 from .geometry import SdfGrid, SdfQuery, query_sdf, read_sdf_cache, write_sdf_cache
@@ -38,7 +39,7 @@ __all__ = [
     "DimensionMismatch", "GelsimError", "InvalidQuery", "LutResolutionMismatch",
     "SdfGrid", "SdfQuery", "query_sdf", "read_sdf_cache", "write_sdf_cache",
     "patch", "unpatch", "SensorArray", "shard_range",
-    "formats", "AugmentConfig", "augment", "render_depth", "DepthImage", "PolyLut", "depth_to_rgb", "monomial_exponents", "synthetic_lut", "to_uint8",
+    "formats", "AugmentConfig", "augment", "BinnedPolyLut", "depth_to_rgb_binned", "render_depth", "DepthImage", "PolyLut", "depth_to_rgb", "monomial_exponents", "synthetic_lut", "to_uint8",
     "TactileCamera", "TactileSensorSpec", "camera_for_sensor", "reference_depth",
     "ForceField", "PenaltyParams", "TactilePointGrid", "compute_force_field", "net_wrench",
     "penalty_forces", "sample_tactile_points",

@@ -53,6 +53,9 @@ SIGNATURES = {
     "tacsl_sensor_step": (c_int, [c_void_p, P, c_int64, c_int, c_int, P, c_void_p, P, c_int, c_int, P, c_int64, P,
                                   c_int64, c_int64, c_int, Penalty, P, P, P, P, c_void_p]),
     "tacsl_net_wrench": (c_int, [P, P, P, c_int64, c_int, c_int, P, P, c_void_p]),
+    "tacsl_binned_lut_create": (c_int, [c_int, P, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p)]),
+    "tacsl_binned_lut_destroy": (None, [c_void_p]),
+    "tacsl_depth_to_rgb_binned": (c_int, [c_void_p, P, c_int64, c_int, c_int, P, P, c_void_p]),
     "tacsl_render_depth": (c_int, [c_void_p, P, P, c_int, c_int, P, c_double, c_double, c_double, c_int, P,
                                    c_int64, P, P, c_void_p]),
 }

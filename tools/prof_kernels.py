@@ -1,5 +1,6 @@
 """One launch of each secondary kernel at benchmark scale, for ncu:
-K3 render_depth, K4 augment, K5 separable filter, K1 obs epilogue."""
+K3 render_depth, K4 augment, K5 separable filter (240x320 and 480x640),
+K1 obs epilogue, K6 binned LUT."""
 import sys
 from pathlib import Path
 
@@ -30,5 +31,13 @@ steps = torch.full((N,), 5, dtype=torch.int64, device=dev)
 augment_device(rgb, cfg, seeds, steps, tactile_rep="diff", nominal=np.float32(lut.coeffs[:, 0]))
 smoothing.gaussian_blur_device(depth, 1.0)
 smoothing.pyr_down_device(depth)
+_, cam5, bg5, _, _ = synthetic.sensor_setup((640, 480))
+d5 = torch.from_numpy(synthetic.depth_batch(cam5, bg5, 32)).to(dev)[torch.arange(N // 4, device=dev) % 32]
+d5 = d5.contiguous()
+smoothing.gaussian_blur_device(d5, 1.0)
+smoothing.pyr_down_device(d5)
+from paper_2408_06506_b200.binned import depth_to_rgb_binned_device, vignetted_lut  # noqa: E402
+u8 = torch.empty(depth.shape + (3,), dtype=torch.uint8, device=dev)
+depth_to_rgb_binned_device(depth, vignetted_lut(lut, (6, 8)), out_u8=u8)
 torch.cuda.synchronize()
 print("ok", N)

@@ -32,6 +32,25 @@ int current_device() {
   return d;
 }
 
+int set_max_dynamic_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, uint64_t>> done;  // kernel -> devices configured (bit mask)
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  uint64_t* mask = nullptr;
+  for (auto& e : done)
+    if (e.first == func) mask = &e.second;
+  if (!mask) {
+    done.emplace_back(func, 0);
+    mask = &done.back().second;
+  }
+  if (dev < 64 && ((*mask >> dev) & 1u)) return TACSL_OK;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(max dynamic shared memory)");
+  if (dev < 64) *mask |= (uint64_t)1 << dev;
+  return TACSL_OK;
+}
+
 int sm_count(int device) {
   static std::mutex mu;
   static std::vector<int> cache;

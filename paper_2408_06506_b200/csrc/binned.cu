@@ -265,7 +265,7 @@ int launch_binned(const tacsl_binned_lut_s* lut, const float* depth, int64_t n, 
   auto kern = vec ? rgb_binned_vec_kernel<DEG> : rgb_binned_kernel<DEG>;
   const size_t smem = binned_smem(lut->bins_y * lut->bins_x, T, lut->width) +
                       (vec ? (size_t)lut->bins_y * lut->bins_x * 3 * T * sizeof(float) : 0);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kBinnedMaxSmem));
+  if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), (int)(2 * kBinnedMaxSmem))) return rc;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBinnedThreads, smem);
   const int QW = (lut->width + 3) / 4;

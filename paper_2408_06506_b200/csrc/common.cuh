@@ -18,6 +18,8 @@ int set_error(int code, const std::string& msg);  // api.cu
 int check_launch(const char* what);                // api.cu: cudaGetLastError -> TACSL_ERR_CUDA
 int sm_count(int device);                           // cached multiProcessorCount
 int current_device();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device); thread-safe
+int set_max_dynamic_smem(const void* func, int bytes);  // api.cu
 
 // ----------------------------------------------------------- device side ---
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {

@@ -166,11 +166,7 @@ template <int NC>
 int launch_filter(const float* in, int64_t n, int H, int W, int Ho, int Wo, int step, const Taps& T, float* out,
                   cudaStream_t stream) {
   auto kern = sep_filter_kernel<NC>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = true;
-  }
+  if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), 227 * 1024)) return rc;
   const size_t smem = ((size_t)kAhead * W + (size_t)(2 * T.radius + 1) * Wo) * sizeof(float);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
@@ -350,14 +346,7 @@ template <int R, int S, int RPT>
 int launch_bulk_filter(const float* in, int64_t n, int H, int W, int Ho, int Wo, const Taps& T, float* out,
                        cudaStream_t stream, FLayout lay) {
   auto kern = sep_bulk_kernel<R, S, RPT>;
-  static std::mutex mu;
-  static bool configured = false;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem) != cudaSuccess)
-      return check_launch("filter: cudaFuncSetAttribute");
-    configured = true;
-  }
+  if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), (int)kFSmem)) return rc;
   const size_t smem = lay.bytes(R, S, W);
   const int threads = bulk_threads_f(Wo, lay.groups);
   int per_sm = 0;
@@ -373,7 +362,7 @@ long score_layout(FLayout lay, int H, int W, int Ho, int Wo) {
   const size_t smem = lay.bytes(R, S, W);
   if (smem > kFSmem) return -1;
   int per_sm = 0;
-  cudaFuncSetAttribute(sep_bulk_kernel<R, S, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem);
+  if (set_max_dynamic_smem(reinterpret_cast<const void*>(sep_bulk_kernel<R, S, RPT>), (int)kFSmem)) return -1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sep_bulk_kernel<R, S, RPT>,
                                                 bulk_threads_f(Wo, lay.groups), smem);
   (void)H;

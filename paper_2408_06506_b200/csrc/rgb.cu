@@ -434,16 +434,11 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
                 const LutParams& L, cudaStream_t stream, const FFArgs<float>* ff = nullptr) {
   auto kern = rgb_bulk_kernel<DEG, RPT, U8, F32, FF>;
   static std::mutex mu;
-  static bool configured = false;
   static std::vector<std::array<int, 4>> cache;  // (H, W, stages) -> groups
   const int QW = W / 4;
   constexpr int kMaxCons = FF ? kMaxThreadsFF : kMaxThreads;
+  if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), (int)kSmemPerSm)) return rc;
   std::lock_guard<std::mutex> lock(mu);
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemPerSm) != cudaSuccess)
-      return check_launch("rgb: cudaFuncSetAttribute");
-    configured = true;
-  }
   int groups = 0;
   if (const char* g = std::getenv("TACSL_RGB_GROUPS")) {
     groups = std::max(1, std::min(std::atoi(g), kMaxCons / QW));

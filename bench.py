@@ -190,7 +190,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(wl, 1),
+        "config": {**workload_config(wl, 1),
+                   "parallelism": f"host CPU: {base.cores} single-threaded worker processes on rank 0 "
+                                  "(oracle port of gelsim's numpy path)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": base.cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -212,10 +214,18 @@ def main():
     from paper_2408_06506_b200.tactile import PenaltyParams
 
     rank, world, local = dist_env()
+    # one process per GPU; TACSL_DIST_BACKEND=gloo lets a multi-rank run share
+    # one GPU as a functional check of the sharding (never a measurement)
+    backend = os.environ.get("TACSL_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -224,7 +234,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -238,7 +248,7 @@ def main():
 
     # ---- inputs resident in HBM: 64 distinct indenter maps tiled to E*S frames
     pool = torch.from_numpy(synthetic.depth_batch(cam, bg, 64, config_id=wl.config_id)).to(dev)
-    idx = torch.arange(E * S, device=dev) % pool.shape[0]
+    idx = (torch.arange(E * S, device=dev) + lo * S) % pool.shape[0]  # this shard's slice of the global job
     depth = pool[idx].reshape(E, S, H, W).contiguous()
     del pool, idx
     obj_all, sen_all = synthetic.peg_states(wl.n_envs, S, config_id=wl.config_id)
@@ -331,11 +341,14 @@ def main():
     e2e = None if args.no_e2e else measure_e2e()
 
     # ---- validation digest across ranks (outside every timed region)
+    from paper_2408_06506_b200.pipeline import frame_checksum
+    dig = frame_checksum(arr.rgb_u8, arr.f_n, arr.f_t).to(coll_dev)  # None-safe
     if world > 1:
-        from paper_2408_06506_b200.pipeline import frame_checksum
-        dig = frame_checksum(arr.rgb_u8, arr.f_n, arr.f_t)  # None-safe
         parts = [torch.zeros_like(dig) for _ in range(world)]
         dist.all_gather(parts, dig)
+        dig = torch.stack(parts).sum(dim=0)
+    validation = {"digest": [float(v) for v in dig.cpu()],
+                  "rule": "sum over ranks of (sum RGB bytes, sum |f_n|, sum |f_t|) of the last step's outputs"}
 
     # ---- roofline of the dominant kernel (K1, or K2 when the step has no RGB) and of the whole step
     peak, peak_src = hbm_peak()
@@ -381,7 +394,7 @@ def main():
                      "k2_force_field_ms": k2_ms, "k2_bytes_per_launch": bytes_["ff"], "fused_ms": kf_ms},
         "gpu_launches": arr.launches_per_step * args.steps,
         "clocks": clocks.summary(),
-        "graph": use_graph, "fused": arr.fused, "overlap": arr.overlap,
+        "graph": use_graph, "fused": arr.fused, "overlap": arr.overlap, "validation": validation,
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -176,3 +176,38 @@ def test_over_2e31_pixels_single_launch():
     assert np.abs(got.astype(int) - ref.astype(int)).max() <= 1
     del d, out
     torch.cuda.empty_cache()
+
+
+def test_config4_shape_fast_kernel_vs_oracle():
+    """Config 4's shapes (80x100 taxels, 128^3 SDF) through the fast K2 path
+    (no kinematics): masks bit-exact, forces within 1e-5 of the oracle, and
+    the full 16384-env batch equals its sampled envs computed alone."""
+    from paper_2408_06506_b200.sensors import TactileSensorSpec
+    from paper_2408_06506_b200.tactile import sample_tactile_points
+    sdf = synthetic.peg_grid((128, 128, 128))
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 80, 100)
+    E4 = 16384
+    obj, sen = synthetic.peg_states(E4, 1, config_id=4)
+    o = torch.from_numpy(obj).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(sen)).cuda()
+    tax = device_taxels(pts, o.device)
+    f_n = torch.empty((E4, 1, 80, 100, 3), dtype=torch.float32, device="cuda")
+    f_t = torch.empty_like(f_n)
+    c = torch.empty((E4, 1, 80, 100), dtype=torch.uint8, device="cuda")
+    force_field_device(sdf, tax, 80, 100, o, s, PenaltyParams(), f_n, f_t, contact=c, n_sensors=1)
+    torch.cuda.synchronize()
+    idx = np.array([0, 1, 4097, 9000, E4 - 1])
+    rn, rt, rk = O.compute_force_field(pts.points, *sdf_tuple(sdf), obj[idx, 0:3], obj[idx, 3:7], obj[idx, 7:10],
+                                       obj[idx, 10:13], sen[idx, 0, 0:3], sen[idx, 0, 3:7], sen[idx, 0, 7:10],
+                                       sen[idx, 0, 10:13])
+    ti = torch.from_numpy(idx).cuda()
+    assert np.array_equal(c[ti, 0].cpu().numpy().astype(bool), rk["d"] < 0)
+    assert (rk["d"] < 0).mean() > 0.02
+    assert vec_close(f_n[ti, 0].cpu().numpy(), rn, 1e-5, atol=1e-9)[0]
+    assert vec_close(f_t[ti, 0].cpu().numpy(), rt, 1e-5, atol=1e-9)[0]
+    sub_n = torch.empty((len(idx), 1, 80, 100, 3), dtype=torch.float32, device="cuda")
+    sub_t = torch.empty_like(sub_n)
+    force_field_device(sdf, tax, 80, 100, o[ti].contiguous(), s[ti].contiguous(), PenaltyParams(), sub_n, sub_t,
+                       n_sensors=1)
+    torch.cuda.synchronize()
+    assert torch.equal(sub_n, f_n[ti]) and torch.equal(sub_t, f_t[ti])

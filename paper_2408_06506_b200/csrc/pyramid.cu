@@ -39,10 +39,32 @@ namespace {
 
 constexpr int kMaxTaps = 33;  // radius <= 16
 
+// Horizontal pass order (both kernels): the taps falling on EVEN input
+// columns and those on ODD columns are summed separately, each in ascending
+// tap order from 0, then added: h = sum_even + sum_odd.  That is the order of
+// the packed-fp32 pipe (FFMA2 lanes = (even column, odd column) pairs of a
+// 16-B shared load); pairs that start one column early carry a zero weight,
+// which changes no value.  we / wo: the weight pairs for a first tap on an
+// even / odd column.
 struct Taps {
   float w[kMaxTaps];
+  float2 we[(kMaxTaps + 1) / 2 + 1];
+  float2 wo[(kMaxTaps + 1) / 2 + 1];
   int radius;
 };
+
+__device__ __forceinline__ float hsum_split(const Taps& T, const float* row, int c, int W, bool clamp) {
+  // generic-kernel form of the even/odd split (see Taps)
+  const int R = T.radius, K = 2 * R + 1;
+  float se = 0.f, so = 0.f;
+  for (int j = 0; j < K; ++j) {
+    const int col = c + j - R;
+    const float v = clamp ? row[min(max(col, 0), W - 1)] : row[col];
+    if (col & 1) so = __fmaf_rn(T.w[j], v, so);
+    else se = __fmaf_rn(T.w[j], v, se);
+  }
+  return se + so;
+}
 
 constexpr int kAhead = 4;       // input rows in flight per CTA (cp.async ring)
 constexpr int kMaxCols = 6;     // output columns per thread (256 threads: Wo <= 1536)
@@ -122,14 +144,7 @@ __global__ void __launch_bounds__(kThreads) sep_filter_kernel(const float* __res
       for (int q = 0; q < NC; ++q) {
         if (!colv[q]) continue;
         const int c = colc[q];
-        float acc = 0.f;
-        if (c - R >= 0 && c + R < W) {  // interior: no border clamps
-          const float* p = row + c - R;
-          for (int j = 0; j < K; ++j) acc = __fmaf_rn(T.w[j], p[j], acc);
-        } else {
-          for (int j = 0; j < K; ++j) acc = __fmaf_rn(T.w[j], row[min(max(c + j - R, 0), W - 1)], acc);
-        }
-        hr[q * kThreads] = acc;
+        hr[q * kThreads] = hsum_split(T, row, c, W, !(c - R >= 0 && c + R < W));
       }
       // emit every output row whose last needed input row has arrived; the
       // ring columns a thread reads are the ones it wrote.  Taps outer,
@@ -184,7 +199,7 @@ int launch_filter(const float* in, int64_t n, int H, int W, int Ho, int Wo, int 
 // Output quads go straight to global memory (one 16-B store per thread and
 // row: a warp writes 512 contiguous bytes), which leaves all of shared
 // memory to the input ring.
-constexpr int kFMaxCons = 512;   // consumer threads per CTA (+ the loader warp)
+constexpr int kFMaxCons = 480;   // consumer threads per CTA (+ the loader warp): 128 registers each
 constexpr int kFMaxStages = 4;
 constexpr size_t kFSmem = 227 * 1024;
 
@@ -295,13 +310,20 @@ __global__ void __launch_bounds__(kFMaxCons + 32, 1)
 #pragma unroll
           for (int i = 0; i < SPAN; ++i) v[i] = row[min(max(xi0 + i, 0), W - 1)];
         }
+        // horizontal: FFMA2 over (even, odd) column pairs of v (v[0] sits on
+        // an even column), even/odd partial sums added at the end (Taps)
         float h[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          float a = 0.f;
+          constexpr int NP = (K + 1) / 2;
+          const int b = OFF - R + S * q;  // first tap's index in v (compile-time)
+          float2 a = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int t = 0; t < K; ++t) a = __fmaf_rn(T.w[t], v[OFF + S * q + t - R], a);
-          h[q] = a;
+          for (int m = 0; m < NP; ++m) {
+            const int i0 = (b & ~1) + 2 * m;
+            a = __ffma2_rn(make_float2(v[i0], v[i0 + 1]), (b & 1) ? T.wo[m] : T.we[m], a);
+          }
+          h[q] = a.x + a.y;
         }
         const float2 h01 = make_float2(h[0], h[1]), h23 = make_float2(h[2], h[3]);
 #pragma unroll
@@ -473,6 +495,14 @@ extern "C" int tacsl_separable_filter(const float* in, int64_t n_images, int hei
   Taps T;
   T.radius = radius;
   for (int k = 0; k < kMaxTaps; ++k) T.w[k] = k < 2 * radius + 1 ? taps[k] : 0.f;
+  {
+    const int K = 2 * radius + 1;
+    auto w = [&](int k) { return k >= 0 && k < K ? T.w[k] : 0.f; };
+    for (int m = 0; m < (kMaxTaps + 1) / 2 + 1; ++m) {
+      T.we[m] = make_float2(w(2 * m), w(2 * m + 1));      // first tap on an even column
+      T.wo[m] = make_float2(w(2 * m - 1), w(2 * m));      // first tap on an odd column: (0, w0), (w1, w2), ...
+    }
+  }
   const size_t smem = ((size_t)kAhead * width + (size_t)(2 * radius + 1) * Wo) * sizeof(float);
   if (smem > 227 * 1024) return set_error(TACSL_ERR_INVALID_ARGUMENT, "filter: image too wide");
   cudaStream_t s = (cudaStream_t)stream;

@@ -263,6 +263,26 @@ def main():
         arr.capture(depth, obj, sen)
     step = arr.replay if use_graph else (lambda: arr.launch(depth, obj, sen))
 
+    def graph_of(fn):
+        """fn's launches as a replayable CUDA graph (per-kernel timing without
+        Python launch overhead between back-to-back launches)."""
+        if not use_graph:
+            return fn
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g.replay
+
+    k1_fn = graph_of(lambda: arr._launch_rgb(depth)) if wl.rgb else None
+    k2_fn = graph_of(lambda: arr._launch_ff(obj, sen)) if wl.ff else None
+    kf_fn = graph_of(lambda: arr._launch_fused(depth, obj, sen)) if arr.fused else None
+
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -282,7 +302,8 @@ def main():
         barrier()
         ms_local = t0.elapsed_time(t1)
 
-        # ---- per-kernel durations, each on its own launching stream
+        # ---- per-kernel durations (each kernel's own graph, replayed on the
+        # current stream -- the stream its launches were captured from)
         def time_kernel(fn, n, segments=5):
             # median over `segments` back-to-back event-timed segments of n launches
             s = torch.cuda.current_stream(dev)
@@ -299,9 +320,9 @@ def main():
             return float(np.median(per))
 
         nk = max(4, args.steps // 5)
-        k1_ms = time_kernel(lambda: arr._launch_rgb(depth), nk) if wl.rgb else None
-        k2_ms = time_kernel(lambda: arr._launch_ff(obj, sen), nk) if wl.ff else None
-        kf_ms = time_kernel(lambda: arr._launch_fused(depth, obj, sen), nk) if arr.fused else None
+        k1_ms = time_kernel(k1_fn, nk) if wl.rgb else None
+        k2_ms = time_kernel(k2_fn, nk) if wl.ff else None
+        kf_ms = time_kernel(kf_fn, nk) if arr.fused else None
     ms = max_over_ranks(ms_local)
     ms_per_step = ms / args.steps
     frames_total = wl.frames  # all ranks together

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
   const int g = is_cons ? (int)threadIdx.x / QW : groups;
   const int x0 = xq << 2;
   const bool at_left = (x0 == 0), at_right = (x0 + 4 >= W);
+  const int loff = at_left ? 0 : -1, roff = at_right ? 3 : 4;
   const float m0 = at_left ? 2.f : 1.f;  // np.gradient one-sided borders are not halved:
   const float m3 = at_right ? 2.f : 1.f; // h = 2*(f1-f0) in the doubled-gradient form
   const int lr0 = g * RPT;
@@ -252,17 +253,18 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
       uint32_t* op = reinterpret_cast<uint32_t*>(out_buf + (size_t)b * out_stage + row_off * 3);
       const int och = L.rep == 2 ? 6 : 3;  // float channels per output pixel
       float* of = F32 ? out_f32 + (((size_t)img * H + r0) * W + row_off) * och : nullptr;
+      // a missing neighbour row / column is read as the pixel itself (the
+      // offsets select it), so there is no select or copy in the row loop
       float4 c = *reinterpret_cast<const float4*>(p);
-      float4 up = (r0 + lr0 > 0) ? *reinterpret_cast<const float4*>(p - W) : c;
+      float4 up = *reinterpret_cast<const float4*>(p - ((r0 + lr0 > 0) ? W : 0));
 #pragma unroll
       for (int j = 0; j < RPT; ++j) {
         if (lr0 + j >= nrows) break;
         const int r = r0 + lr0 + j;
-        const float4 dn = (r < H - 1) ? *reinterpret_cast<const float4*>(p + W) : c;
-        // left/right neighbours of the quad; the reads at the image's side
-        // borders land inside the stage buffer and are replaced by c.x / c.w
-        const float left = at_left ? c.x : p[-1];
-        const float right = at_right ? c.w : p[4];
+        const float4 dn = *reinterpret_cast<const float4*>(p + ((r < H - 1) ? W : 0));
+        // left/right neighbours of the quad (c.x / c.w at the side borders)
+        const float left = p[loff];
+        const float right = p[roff];
         // doubled gradients h = 2g (coefficients carry the 2^-(i+j))
         float2 hy01 = __fadd2_rn(make_float2(dn.x, dn.y), make_float2(-up.x, -up.y));
         float2 hy23 = __fadd2_rn(make_float2(dn.z, dn.w), make_float2(-up.z, -up.w));

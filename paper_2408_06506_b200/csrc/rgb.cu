@@ -119,7 +119,7 @@ struct Layout {
 //   empty[s] : every consumer warp has its rows of stage s in registers
 //   ready[b] : every consumer warp wrote its part of output tile b
 //   ofree[b] : the bulk store of tile b has finished reading it
-template <int DEG, int RPT, bool U8, bool F32, bool FF>
+template <int DEG, int RPT, bool U8, bool F32, bool FF, bool COPY_ONLY = false>
 __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMaxThreads + 64, 1) rgb_bulk_kernel(const float* __restrict__ depth,
                                                                     int64_t n_images, int H, int W, int groups,
                                                                     int stages, uint8_t* __restrict__ out_u8,
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
         }
         const float2 hx01 = make_float2((c.y - left) * m0, c.z - c.x);
         const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
-        if (bulk_store & 2) {  // TACSL_RGB_DEBUG_COPY: data movement only (roofline experiments)
+        if constexpr (COPY_ONLY) {  // TACSL_RGB_DEBUG_COPY: data movement only (roofline experiments)
           if (U8) {
             op[0] = __float_as_uint(hx01.x);
             op[1] = __float_as_uint(hy01.y);
@@ -481,12 +481,18 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
   const int bands = (H + lay.band - 1) / lay.band;
   const int64_t units = n * bands;
   int64_t grid = std::min<int64_t>(units, (int64_t)sm_count(current_device()) * per_sm);
-  int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
-  if (std::getenv("TACSL_RGB_DEBUG_COPY")) bulk_store |= 2;
+  const int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
   FFArgs<float> F{};
   if (FF) F = *ff;
-  kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
-                                                  bulk_store, F);
+  if (std::getenv("TACSL_RGB_DEBUG_COPY")) {  // same pipeline, shading replaced by stores of the inputs
+    auto copy_kern = rgb_bulk_kernel<DEG, RPT, U8, F32, FF, true>;
+    if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(copy_kern), (int)kSmemPerSm)) return rc;
+    copy_kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
+                                                         bulk_store, F);
+  } else {
+    kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
+                                                    bulk_store, F);
+  }
   return check_launch("rgb_bulk_kernel");
 }
 

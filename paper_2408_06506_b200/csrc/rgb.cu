@@ -119,7 +119,7 @@ struct Layout {
 //   empty[s] : every consumer warp has its rows of stage s in registers
 //   ready[b] : every consumer warp wrote its part of output tile b
 //   ofree[b] : the bulk store of tile b has finished reading it
-template <int DEG, int RPT, bool U8, bool F32, bool FF, bool COPY_ONLY = false>
+template <int DEG, int RPT, bool U8, bool F32, bool FF>
 __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMaxThreads + 64, 1) rgb_bulk_kernel(const float* __restrict__ depth,
                                                                     int64_t n_images, int H, int W, int groups,
                                                                     int stages, uint8_t* __restrict__ out_u8,
@@ -274,55 +274,47 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
         }
         const float2 hx01 = make_float2((c.y - left) * m0, c.z - c.x);
         const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
-        if constexpr (COPY_ONLY) {  // TACSL_RGB_DEBUG_COPY: data movement only (roofline experiments)
-          if (U8) {
-            op[0] = __float_as_uint(hx01.x);
-            op[1] = __float_as_uint(hy01.y);
-            op[2] = __float_as_uint(hx23.y);
+        const float2 r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
+        const float2 g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
+        const float2 b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
+        const float2 r23 = poly2_sat<DEG>(L.c[0], hx23, hy23);
+        const float2 g23 = poly2_sat<DEG>(L.c[1], hx23, hy23);
+        const float2 b23 = poly2_sat<DEG>(L.c[2], hx23, hy23);
+        if (U8) {
+          // pixel order p0..p3, channel-interleaved: (r0 g0 b0 r1)(g1 b1 r2 g2)(b2 r3 g3 b3)
+          const float2 qa = q8x2(make_float2(r01.x, g01.x));
+          const float2 qb = q8x2(make_float2(b01.x, r01.y));
+          const float2 qc = q8x2(make_float2(g01.y, b01.y));
+          const float2 qd = q8x2(make_float2(r23.x, g23.x));
+          const float2 qe = q8x2(make_float2(b23.x, r23.y));
+          const float2 qf = q8x2(make_float2(g23.y, b23.y));
+          op[0] = __byte_perm(__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040),
+                              __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040), 0x5410);
+          op[1] = __byte_perm(__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040),
+                              __byte_perm(__float_as_uint(qd.x), __float_as_uint(qd.y), 0x0040), 0x5410);
+          op[2] = __byte_perm(__byte_perm(__float_as_uint(qe.x), __float_as_uint(qe.y), 0x0040),
+                              __byte_perm(__float_as_uint(qf.x), __float_as_uint(qf.y), 0x0040), 0x5410);
+        }
+        if (F32) {
+          float4* o = reinterpret_cast<float4*>(of);
+          const float n0 = L.nominal[0], n1 = L.nominal[1], n2 = L.nominal[2];
+          if (L.rep == 0) {  // "color" (envs/peg_tasks.py:445, .astype(float32))
+            o[0] = make_float4(r01.x, g01.x, b01.x, r01.y);
+            o[1] = make_float4(g01.y, b01.y, r23.x, g23.x);
+            o[2] = make_float4(b23.x, r23.y, g23.y, b23.y);
+          } else if (L.rep == 1) {  // "diff": rgb - nominal (peg_tasks.py:453-454)
+            o[0] = make_float4(r01.x - n0, g01.x - n1, b01.x - n2, r01.y - n0);
+            o[1] = make_float4(g01.y - n1, b01.y - n2, r23.x - n0, g23.x - n1);
+            o[2] = make_float4(b23.x - n2, r23.y - n0, g23.y - n1, b23.y - n2);
+          } else {  // "concat": [rgb, nominal] on the channel axis (peg_tasks.py:455-458)
+            o[0] = make_float4(r01.x, g01.x, b01.x, n0);
+            o[1] = make_float4(n1, n2, r01.y, g01.y);
+            o[2] = make_float4(b01.y, n0, n1, n2);
+            o[3] = make_float4(r23.x, g23.x, b23.x, n0);
+            o[4] = make_float4(n1, n2, r23.y, g23.y);
+            o[5] = make_float4(b23.y, n0, n1, n2);
           }
-        } else {
-          const float2 r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
-          const float2 g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
-          const float2 b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
-          const float2 r23 = poly2_sat<DEG>(L.c[0], hx23, hy23);
-          const float2 g23 = poly2_sat<DEG>(L.c[1], hx23, hy23);
-          const float2 b23 = poly2_sat<DEG>(L.c[2], hx23, hy23);
-          if (U8) {
-            // pixel order p0..p3, channel-interleaved: (r0 g0 b0 r1)(g1 b1 r2 g2)(b2 r3 g3 b3)
-            const float2 qa = q8x2(make_float2(r01.x, g01.x));
-            const float2 qb = q8x2(make_float2(b01.x, r01.y));
-            const float2 qc = q8x2(make_float2(g01.y, b01.y));
-            const float2 qd = q8x2(make_float2(r23.x, g23.x));
-            const float2 qe = q8x2(make_float2(b23.x, r23.y));
-            const float2 qf = q8x2(make_float2(g23.y, b23.y));
-            op[0] = __byte_perm(__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040),
-                                __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040), 0x5410);
-            op[1] = __byte_perm(__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040),
-                                __byte_perm(__float_as_uint(qd.x), __float_as_uint(qd.y), 0x0040), 0x5410);
-            op[2] = __byte_perm(__byte_perm(__float_as_uint(qe.x), __float_as_uint(qe.y), 0x0040),
-                                __byte_perm(__float_as_uint(qf.x), __float_as_uint(qf.y), 0x0040), 0x5410);
-          }
-          if (F32) {
-            float4* o = reinterpret_cast<float4*>(of);
-            const float n0 = L.nominal[0], n1 = L.nominal[1], n2 = L.nominal[2];
-            if (L.rep == 0) {  // "color" (envs/peg_tasks.py:445, .astype(float32))
-              o[0] = make_float4(r01.x, g01.x, b01.x, r01.y);
-              o[1] = make_float4(g01.y, b01.y, r23.x, g23.x);
-              o[2] = make_float4(b23.x, r23.y, g23.y, b23.y);
-            } else if (L.rep == 1) {  // "diff": rgb - nominal (peg_tasks.py:453-454)
-              o[0] = make_float4(r01.x - n0, g01.x - n1, b01.x - n2, r01.y - n0);
-              o[1] = make_float4(g01.y - n1, b01.y - n2, r23.x - n0, g23.x - n1);
-              o[2] = make_float4(b23.x - n2, r23.y - n0, g23.y - n1, b23.y - n2);
-            } else {  // "concat": [rgb, nominal] on the channel axis (peg_tasks.py:455-458)
-              o[0] = make_float4(r01.x, g01.x, b01.x, n0);
-              o[1] = make_float4(n1, n2, r01.y, g01.y);
-              o[2] = make_float4(b01.y, n0, n1, n2);
-              o[3] = make_float4(r23.x, g23.x, b23.x, n0);
-              o[4] = make_float4(n1, n2, r23.y, g23.y);
-              o[5] = make_float4(b23.y, n0, n1, n2);
-            }
-            of += (size_t)W * och;
-          }
+          of += (size_t)W * och;
         }
         up = c;
         c = dn;
@@ -484,15 +476,8 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
   const int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
   FFArgs<float> F{};
   if (FF) F = *ff;
-  if (std::getenv("TACSL_RGB_DEBUG_COPY")) {  // same pipeline, shading replaced by stores of the inputs
-    auto copy_kern = rgb_bulk_kernel<DEG, RPT, U8, F32, FF, true>;
-    if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(copy_kern), (int)kSmemPerSm)) return rc;
-    copy_kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
-                                                         bulk_store, F);
-  } else {
-    kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
-                                                    bulk_store, F);
-  }
+  kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
+                                                  bulk_store, F);
   return check_launch("rgb_bulk_kernel");
 }
 

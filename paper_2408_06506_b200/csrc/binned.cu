@@ -148,7 +148,7 @@ __device__ __forceinline__ uint32_t pack4(float2 a, float2 b) {
                      __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040), 0x5410);
 }
 
-template <int DEG>
+template <int DEG, bool ALIGNED>  // ALIGNED: every bin edge on a multiple of 4 columns (no straddling quads)
 __global__ void __launch_bounds__(kBinnedThreads) rgb_binned_vec_kernel(const float* __restrict__ depth, int64_t n,
                                                                         int H, int W, int bins_y, int bins_x,
                                                                         const float* __restrict__ coeffs,
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kBinnedThreads) rgb_binned_vec_kernel(const fl
   const bool at_left = x0 == 0, at_right = x0 + 4 >= W;
   const float m0 = at_left ? 2.f : 1.f, m3 = at_right ? 2.f : 1.f;
   const int b0 = xbin[x0], b1 = xbin[x0 + 1], b2 = xbin[x0 + 2], b3 = xbin[x0 + 3];
-  const bool one_bin = b0 == b3;
+  const bool one_bin = ALIGNED || b0 == b3;
   const int bands = (H + kRows - 1) / kRows;
   const int64_t units = n * bands;
   for (int64_t u = (int64_t)blockIdx.x * groups + g; u < units; u += (int64_t)gridDim.x * groups) {
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kBinnedThreads) rgb_binned_vec_kernel(const fl
           v01[ch] = poly2_sat_r<DEG>(cp, hx01, hy01);
           v23[ch] = poly2_sat_r<DEG>(cp, hx23, hy23);
         }
-      } else {  // the quad straddles a bin edge: a set per pixel pair, mixed only inside a pair
+      } else if constexpr (!ALIGNED) {  // the quad straddles a bin edge: a set per pixel pair, mixed only inside a pair
         const float2* s0 = dup + (size_t)(yb + b0) * 3 * T;
         const float2* s1 = dup + (size_t)(yb + b1) * 3 * T;
         const float2* s2 = dup + (size_t)(yb + b2) * 3 * T;
@@ -262,7 +262,13 @@ int launch_binned(const tacsl_binned_lut_s* lut, const float* depth, int64_t n, 
   const bool vec = W % 4 == 0 && W / 4 <= kBinnedThreads && (reinterpret_cast<uintptr_t>(depth) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(u8) & 3) == 0 && (reinterpret_cast<uintptr_t>(f32) & 15) == 0 &&
                    !std::getenv("TACSL_BINNED_SCALAR");
-  auto kern = vec ? rgb_binned_vec_kernel<DEG> : rgb_binned_kernel<DEG>;
+  bool aligned = true;  // every x-bin edge floor(b * W / bins_x) on a multiple of 4
+  for (int b = 1; b < lut->bins_x && aligned; ++b) {
+    const int64_t edge = ((int64_t)b * W + lut->bins_x - 1) / lut->bins_x;  // first column of bin b
+    aligned = edge % 4 == 0;
+  }
+  auto kern = !vec ? rgb_binned_kernel<DEG> : aligned ? rgb_binned_vec_kernel<DEG, true>
+                                                      : rgb_binned_vec_kernel<DEG, false>;
   const size_t smem = binned_smem(lut->bins_y * lut->bins_x, T, lut->width) +
                       (vec ? (size_t)lut->bins_y * lut->bins_x * 3 * T * sizeof(float) : 0);
   if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), (int)(2 * kBinnedMaxSmem))) return rc;

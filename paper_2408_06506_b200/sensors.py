@@ -3,8 +3,9 @@
 Mirrors the parts of ``gelsim.sensors`` (sensors.py:26-50) and
 ``gelsim.render.camera`` (camera.py:13-66) that fix the hot path's shapes:
 the active area, the image size, the pinhole intrinsics and the flat-pad
-membrane depth.  Curved gels (ray casts against a surface mesh) are asset
-preparation and out of scope.
+membrane depth (the reference's ray cast against its two-triangle pad mesh,
+restated so the background is bit-identical).  Curved gels (ray casts
+against an arbitrary surface mesh) are asset preparation and out of scope.
 """
 from __future__ import annotations
 
@@ -66,9 +67,56 @@ def camera_for_sensor(sensor: TactileSensorSpec) -> TactileCamera:
                          width=W, height=H, near=sensor.near, far=sensor.far)
 
 
+def flat_pad_triangles(active_area, skirt: float = 0.002) -> np.ndarray:
+    """The flat pad's gel surface: two triangles at z = 0 covering the active
+    area plus a skirt, (2, 3, 3) (sensors.py:17-23 flat_pad_mesh)."""
+    hx = active_area[0] / 2.0 + skirt
+    hy = active_area[1] / 2.0 + skirt
+    v = np.array([[-hx, -hy, 0.0], [hx, -hy, 0.0], [hx, hy, 0.0], [-hx, hy, 0.0]])
+    return v[np.array([[0, 1, 2], [0, 2, 3]])]
+
+
+def _cross(a, b):
+    """np.cross component order: each product rounded, then subtracted."""
+    return np.stack([a[..., 1] * b[..., 2] - a[..., 2] * b[..., 1],
+                     a[..., 2] * b[..., 0] - a[..., 0] * b[..., 2],
+                     a[..., 0] * b[..., 1] - a[..., 1] * b[..., 0]], axis=-1)
+
+
+def _dot(a, b):
+    """3-term dot product summed left to right (np.einsum's order)."""
+    return (a[..., 0] * b[..., 0] + a[..., 1] * b[..., 1]) + a[..., 2] * b[..., 2]
+
+
+def ray_triangles_t(origins, directions, triangles) -> np.ndarray:
+    """Nearest non-negative hit parameter per ray over a triangle list, +inf on
+    a miss: Moller-Trumbore with the reference's tolerances and operation order
+    (geometry/mesh.py:166-193), so the membrane depth is bit-identical."""
+    o = np.asarray(origins, dtype=np.float64)[:, None]      # (R, 1, 3)
+    d = np.asarray(directions, dtype=np.float64)[:, None]
+    tri = np.asarray(triangles, dtype=np.float64)
+    v0, e1, e2 = tri[:, 0], tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0]
+    pvec = _cross(d, e2[None])
+    det = _dot(pvec, e1[None])
+    ok = np.abs(det) > 1e-14
+    inv = np.where(ok, 1.0 / np.where(ok, det, 1.0), 0.0)
+    tvec = o - v0[None]
+    u = _dot(tvec, pvec) * inv
+    qvec = _cross(tvec, e1[None])
+    v = _dot(d, qvec) * inv
+    t = _dot(e2[None], qvec) * inv
+    hit = ok & (u >= -1e-12) & (v >= -1e-12) & (u + v <= 1 + 1e-12) & (t >= 0)
+    return np.where(hit, t, np.inf).min(axis=1)
+
+
 def reference_depth(camera: TactileCamera, sensor: TactileSensorSpec | None = None) -> np.ndarray:
-    """Membrane depth per pixel for the flat pad at z = 0: the ray parameter
-    where the ray meets the gel plane, clipped to [near, far] (camera.py:56-66)."""
-    d = camera.rays()
-    t = -camera.pos[2] / d[..., 2]
-    return np.clip(t, camera.near, camera.far)
+    """Membrane depth per pixel (camera.py:56-66): the rays cast against the
+    flat pad's surface triangles, misses at the far plane, clipped to
+    [near, far].  Bit-identical to the reference's (which casts against the
+    same two-triangle mesh)."""
+    sensor = sensor or TactileSensorSpec(image_size=(camera.width, camera.height))
+    dirs = camera.rays().reshape(-1, 3)
+    origins = np.broadcast_to(camera.pos, dirs.shape)
+    t = ray_triangles_t(origins, dirs, flat_pad_triangles(sensor.active_area))
+    t = np.where(np.isfinite(t), t, camera.far)
+    return np.clip(t, camera.near, camera.far).reshape(camera.height, camera.width)

@@ -18,6 +18,8 @@ Fixtures:
                  plus one unbatched call
   penalty.npz    penalty_forces on the seed-11 draws of
                  test_tactile_field.py:153-168
+  env.npz        PegEnvBatch tactile image / force-field observations with
+                 augmentation and their inputs (``make_golden.py env``)
 """
 from __future__ import annotations
 
@@ -248,7 +250,64 @@ def make_augment():
     np.savez_compressed(HERE / "augment.npz", **out)
 
 
-if __name__ == "__main__":
+def make_env():
+    """PegEnvBatch tactile observations (envs/peg_tasks.py:434-477) after a
+    reset and two zero-action steps, with augmentation and the "diff"
+    representation, plus every input needed to recompute them on the device:
+    the per-sensor depth maps the env renders (render_depth, as
+    _tactile_images does), the peg / sensor states _tactile_ff passes, the
+    per-env augmentation seeds and step counts, the LUT and taxel grid."""
+    from gelsim.envs.base import EnvConfig
+    from gelsim.envs.peg_tasks import PEG, PegEnvBatch
+    from gelsim.render.augment import AugmentConfig
+    from gelsim.transforms import quat_conj, quat_mul, quat_rotate_inv
+
+    aug = AugmentConfig(shift_px=1.5, zoom=(0.95, 1.08), brightness=0.05, contrast=(0.9, 1.1),
+                        saturation=(0.85, 1.15), hue=0.02, channel_permutation=True, step_brightness=0.01,
+                        step_contrast=(0.98, 1.02), step_saturation=(0.97, 1.03), step_hue=0.005, seed=7)
+    E = 6
+    cfg = EnvConfig(num_envs=E, seed=3, tactile_rep="diff", augment=aug,
+                    obs_modalities=("tactile_img", "tactile_ff"))
+    env = PegEnvBatch(cfg)
+    env.reset()
+    for _ in range(2):
+        env.step(np.zeros((E, 6)))
+    images = env._tactile_images()
+    ff = env._tactile_ff()
+    depth, sen, rel_p, rel_q = [], [], [], []
+    for s_idx in range(2):
+        pos, quat = env._sensor_world_pose(s_idx)
+        rel_pos = quat_rotate_inv(quat, env.bodies.pos[:, PEG] - pos)
+        rel_quat = quat_mul(quat_conj(quat), env.bodies.quat[:, PEG])
+        rel_p.append(rel_pos)
+        rel_q.append(rel_quat)
+        depth.append(render_depth(env.camera, env.peg_sdf, rel_pos, rel_quat, env.background).values)
+        v, w = env._sensor_world_velocity(pos)
+        sen.append(np.concatenate([pos, quat, v, w], axis=1))
+    obj = np.concatenate([env.bodies.pos[:, PEG], env.bodies.quat[:, PEG], env.bodies.linvel[:, PEG],
+                          env.bodies.angvel[:, PEG]], axis=1)
+    g = env.peg_sdf  # the env's own build_sdf peg (32x32x64, float64)
+    p = cfg.penalty
+    np.savez_compressed(
+        HERE / "env.npz", images=images, ff=ff, depth=np.stack(depth, axis=1), obj=obj,
+        rel_pos=np.stack(rel_p, axis=1), rel_quat=np.stack(rel_q, axis=1), background=env.background,
+        cam_dirs=env.camera.rays(),
+        sen=np.stack(sen, axis=1), seeds=(env.env_seeds * 1000003 + env.episode).astype(np.int64),
+        steps=env.step_count.astype(np.int64), lut_coeffs=env.lut.coeffs, lut_degree=env.lut.degree,
+        image_size=np.array(cfg.tactile_image_size), ff_points=env.ff_grid.points,
+        penalty=np.array([p.k_n, p.k_d, p.k_t, p.mu]),
+        sdf_origin=np.asarray(g.origin), sdf_spacing=np.float64(g.spacing), sdf_dims=np.array(g.dims),
+        sdf_values=g.values, sdf_gradients=g.gradients,
+        aug=np.array([aug.shift_px, aug.zoom[0], aug.zoom[1], aug.brightness, aug.contrast[0], aug.contrast[1],
+                      aug.saturation[0], aug.saturation[1], aug.hue, float(aug.channel_permutation),
+                      aug.step_brightness, aug.step_contrast[0], aug.step_contrast[1], aug.step_saturation[0],
+                      aug.step_saturation[1], aug.step_hue, aug.seed]))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    for name in sys.argv[1:]:
+        globals()[f"make_{name}"]()
+elif __name__ == "__main__":
     make_augment()
     make_rgb()
     g = peg_grid_reference()
@@ -257,5 +316,6 @@ if __name__ == "__main__":
     make_penalty()
     make_depth(g)
     make_formats()
+    make_env()
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -1,0 +1,75 @@
+"""The whole tactile observation chain of the reference env, against the
+env itself: tests/golden/env.npz holds PegEnvBatch._tactile_images /
+_tactile_ff outputs (envs/peg_tasks.py:434-477) recorded by running the
+REFERENCE env (6 envs x 2 fingers, augmentation on, "diff" representation,
+its own build_sdf peg) plus the inputs the env used.  Here:
+
+* K3 render_depth of the env's relative peg poses reproduces the env's depth
+  maps bit for bit;
+* TactileObservations (K1 float epilogue + K4 augmentation + K2 packed
+  force-field observation) reproduces the observations: images within one
+  uint8 step (the fp32 shading differs from the reference's fp64 by <= 1e-6
+  and the HSV round trip passes that through), force-field observation within
+  1e-5 relative with the contact mask exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, vec_close
+from paper_2408_06506_b200 import AugmentConfig
+from paper_2408_06506_b200.depth import render_depth
+from paper_2408_06506_b200.geometry import SdfGrid
+from paper_2408_06506_b200.pipeline import TactileObservations
+from paper_2408_06506_b200.render import PolyLut
+from paper_2408_06506_b200.sensors import TactileSensorSpec, camera_for_sensor, reference_depth
+from paper_2408_06506_b200.tactile import PenaltyParams, TactilePointGrid
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    z = dict(np.load(GOLDEN / "env.npz"))
+    z["sdf"] = SdfGrid(origin=z["sdf_origin"], spacing=float(z["sdf_spacing"]), dims=tuple(int(v) for v in z["sdf_dims"]),
+                       values=z["sdf_values"], gradients=z["sdf_gradients"])
+    z["lut"] = PolyLut(degree=int(z["lut_degree"]), coeffs=z["lut_coeffs"],
+                       image_size=tuple(int(v) for v in z["image_size"]))
+    return z
+
+
+def test_env_depth_bit_exact(env):
+    W, H = (int(v) for v in env["image_size"])
+    spec = TactileSensorSpec(image_size=(W, H))
+    cam = camera_for_sensor(spec)
+    bg = reference_depth(cam, spec)
+    for s in range(2):
+        d = render_depth(cam, env["sdf"], env["rel_pos"][:, s], env["rel_quat"][:, s], bg)
+        assert np.array_equal(d.values, env["depth"][:, s]), s
+
+
+def test_env_tactile_observations(env):
+    a = env["aug"]
+    cfg = AugmentConfig(shift_px=a[0], zoom=(a[1], a[2]), brightness=a[3], contrast=(a[4], a[5]),
+                        saturation=(a[6], a[7]), hue=a[8], channel_permutation=bool(a[9]), step_brightness=a[10],
+                        step_contrast=(a[11], a[12]), step_saturation=(a[13], a[14]), step_hue=a[15],
+                        seed=int(a[16]))
+    pts = env["ff_points"]
+    grid = TactilePointGrid(points=pts, rest_normals=np.broadcast_to([0.0, 0.0, 1.0], pts.shape).copy(),
+                            spacing=(float(pts[0, 1, 0] - pts[0, 0, 0]), float(pts[1, 0, 1] - pts[0, 0, 1])))
+    E = env["obj"].shape[0]
+    obs = TactileObservations(env["lut"], env["sdf"], grid, PenaltyParams(*env["penalty"]), E, 2, tactile_rep="diff",
+                              augment=cfg)
+    depth = torch.from_numpy(env["depth"].astype(np.float32)).cuda()
+    images, ff = obs(depth, torch.from_numpy(env["obj"]).cuda(), torch.from_numpy(np.ascontiguousarray(env["sen"])).cuda(),
+                     episode_seeds=env["seeds"], step_indices=env["steps"])
+    torch.cuda.synchronize()
+    got = images.cpu().numpy()
+    ref = env["images"]
+    diff = np.abs(got - ref)
+    assert diff.max() <= 1.0 / 255.0, diff.max()
+    assert (diff > 1e-5).mean() < 0.01, (diff > 1e-5).mean()
+    f = ff.cpu().numpy()
+    assert np.array_equal(np.abs(f).sum(-1) > 0, np.abs(env["ff"]).sum(-1) > 0)
+    assert (np.abs(env["ff"]).sum(-1) > 0).mean() > 0.05
+    assert vec_close(f, env["ff"], 1e-5, atol=1e-7)[0]

@@ -87,3 +87,15 @@ def test_analytic_grid_layout_matches_build_sdf_rule():
 def test_polylut_validation():
     with pytest.raises(ValueError):
         PolyLut(degree=5, coeffs=np.zeros((3, 21)), image_size=(8, 8))
+
+
+def test_reference_depth_bit_identical_to_env_background():
+    """The membrane depth (ray cast against the pad's two triangles) equals
+    the background the reference env computed (tests/golden/env.npz)."""
+    from conftest import GOLDEN
+    from paper_2408_06506_b200.sensors import TactileSensorSpec, camera_for_sensor, reference_depth
+    z = np.load(GOLDEN / "env.npz")
+    spec = TactileSensorSpec(image_size=tuple(int(v) for v in z["image_size"]))
+    cam = camera_for_sensor(spec)
+    assert np.array_equal(cam.rays(), z["cam_dirs"])
+    assert np.array_equal(reference_depth(cam, spec), z["background"])

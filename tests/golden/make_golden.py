@@ -20,6 +20,7 @@ Fixtures:
                  test_tactile_field.py:153-168
   env.npz        PegEnvBatch tactile image / force-field observations with
                  augmentation and their inputs (``make_golden.py env``)
+  scene.npz      shape_sensing_scene end to end (``make_golden.py scene``)
 """
 from __future__ import annotations
 
@@ -304,9 +305,28 @@ def make_env():
                       aug.step_saturation[1], aug.step_hue, aug.seed]))
 
 
+def make_scene(grid):
+    """envs/scenes.py:27-57 shape_sensing_scene end to end (render_depth ->
+    depth_to_rgb, compute_force_field) for four batched peg presses on the
+    reference-built 16x16x32 peg grid of sdf.npz."""
+    from gelsim.envs.scenes import shape_sensing_scene
+    from gelsim.transforms import quat_from_axis_angle
+
+    rng = np.random.default_rng(np.random.SeedSequence((20240812, 77)))
+    E = 4
+    pos = np.stack([rng.uniform(-0.002, 0.002, E), rng.uniform(-0.002, 0.002, E),
+                    0.008 - rng.uniform(0.0002, 0.0009, E)], axis=1)
+    ang = np.pi / 2 + rng.uniform(-0.1, 0.1, E)
+    quat = quat_from_axis_angle(np.tile([0.0, 1.0, 0.0], (E, 1)), ang)
+    rgb, fld = shape_sensing_scene(grid, pos, quat, num_envs=E)
+    np.savez_compressed(HERE / "scene.npz", press_pos=pos, press_quat=quat, rgb=rgb.astype(np.float32),
+                        f_n=fld.f_n, f_t=fld.f_t)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     for name in sys.argv[1:]:
-        globals()[f"make_{name}"]()
+        fn = globals()[f"make_{name}"]
+        fn(peg_grid_reference()) if name in ("sdf", "ff", "depth", "scene") else fn()
 elif __name__ == "__main__":
     make_augment()
     make_rgb()
@@ -317,5 +337,6 @@ elif __name__ == "__main__":
     make_depth(g)
     make_formats()
     make_env()
+    make_scene(g)
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -73,3 +73,29 @@ def test_env_tactile_observations(env):
     assert np.array_equal(np.abs(f).sum(-1) > 0, np.abs(env["ff"]).sum(-1) > 0)
     assert (np.abs(env["ff"]).sum(-1) > 0).mean() > 0.05
     assert vec_close(f, env["ff"], 1e-5, atol=1e-7)[0]
+
+
+def test_shape_sensing_scene_end_to_end(golden_grid):
+    """envs/scenes.py:27-57 shape_sensing_scene recomputed with this package's
+    drop-ins (render_depth -> depth_to_rgb, compute_force_field) against the
+    reference's own output (tests/golden/scene.npz)."""
+    from oracle.gelsim_oracle import to_uint8
+    from paper_2408_06506_b200.render import depth_to_rgb, synthetic_lut
+    from paper_2408_06506_b200.sensors import IDENTITY_QUAT
+    from paper_2408_06506_b200.tactile import compute_force_field, sample_tactile_points
+    z = np.load(GOLDEN / "scene.npz")
+    spec = TactileSensorSpec()
+    cam = camera_for_sensor(spec)
+    bg = reference_depth(cam, spec)
+    lut = synthetic_lut(spec.image_size)
+    depth = render_depth(cam, golden_grid, z["press_pos"], z["press_quat"], bg)
+    rgb = depth_to_rgb(depth, lut)
+    assert rgb.dtype == np.float64 and rgb.shape == z["rgb"].shape
+    assert np.abs(rgb - z["rgb"]).max() < 1e-5
+    assert np.abs(to_uint8(rgb).astype(int) - to_uint8(z["rgb"].astype(np.float64)).astype(int)).max() <= 1
+    zeros = np.zeros_like(z["press_pos"])
+    fld = compute_force_field(sample_tactile_points(spec, 10, 14), golden_grid, z["press_pos"], z["press_quat"],
+                              zeros, zeros, np.zeros(3), IDENTITY_QUAT, np.zeros(3), np.zeros(3), PenaltyParams())
+    assert np.array_equal(np.linalg.norm(fld.f_n, axis=-1) > 0, np.linalg.norm(z["f_n"], axis=-1) > 0)
+    assert vec_close(fld.f_n, z["f_n"], 1e-5)[0]
+    assert vec_close(fld.f_t, z["f_t"], 1e-5)[0]

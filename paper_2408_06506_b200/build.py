@@ -49,20 +49,43 @@ def needs_rebuild() -> bool:
 
 
 def build(verbose: bool = False, force: bool = False) -> Path:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file),
+    then link the shared library; the .so is replaced atomically."""
     if not force and not needs_rebuild():
         return LIB_PATH
+    from concurrent.futures import ThreadPoolExecutor
+
     nvcc = nvcc_path()
-    tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-shared",
-           "-o", str(tmp), *map(str, sources())]
+    objdir = PKG / "build_obj"
+    objdir.mkdir(exist_ok=True)
+    flags = [*ARCH_FLAGS, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
+        flags.insert(0, "-Xptxas=-v")
+
+    def compile_one(src: Path):
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc, *flags, "-c", str(src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    srcs = list(sources())
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    failed = False
+    for obj, res in results:
+        if verbose or res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+        failed |= res.returncode != 0
+    if failed:
+        raise RuntimeError(f"nvcc failed building {LIB_NAME}")
+    tmp = LIB_PATH.with_suffix(".so.tmp")
+    cmd = [nvcc, *ARCH_FLAGS, "-shared", "-o", str(tmp), *(str(o) for o, _ in results)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}) building {LIB_NAME}")
+        raise RuntimeError(f"nvcc failed ({res.returncode}) linking {LIB_NAME}")
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -87,6 +87,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}) linking {LIB_NAME}")
     os.replace(tmp, LIB_PATH)
+    shutil.rmtree(objdir, ignore_errors=True)
     return LIB_PATH
 
 

@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     p.add_argument("--e2e-chunks", type=int, default=64, help="env chunks pipelined over H2D / compute / D2H")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample length")
+    p.add_argument("--envs", type=int, default=None,
+                   help="override the config's env count (experiments, e.g. one GPU's share at N GPUs)")
     return p.parse_args()
 
 
@@ -239,6 +241,9 @@ def main():
         return float(t.item())
 
     wl = synthetic.CONFIGS[args.config]
+    if args.envs:
+        import dataclasses
+        wl = dataclasses.replace(wl, n_envs=args.envs)
     lo, hi = shard_range(wl.n_envs, rank, world)
     E, S = hi - lo, wl.n_sensors
     W, H = wl.image_size

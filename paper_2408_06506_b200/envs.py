@@ -1,0 +1,115 @@
+"""Batched replacements of the reference env's tactile observation methods
+(the caller of the hot path):
+
+    PegEnvBatch._tactile_images  envs/peg_tasks.py:434-459
+    PegEnvBatch._tactile_ff      envs/peg_tasks.py:461-477
+
+The reference loops over the two fingers and, for augmentation, over every
+env in Python, calling render_depth / depth_to_rgb / augment /
+compute_force_field per slice.  Here one call per step does both fingers of
+all envs: K3 renders the 2E depth maps, K1 shades them (float epilogue), K4
+applies the per-(env, episode, step) augmentation, K2 writes the packed
+[f_n.z, f_t.x, f_t.y] observation -- each ONE launch.  ``patch()`` binds
+these as the env's methods; they read the same env attributes the reference
+methods read and return the same float32 numpy arrays.
+
+Per-env device state (ray table, SDF / LUT handles, taxels, output buffers)
+is cached on the env object under ``_tacsl``.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device
+from .augment import augment_device
+from .depth import RayTable, env_params, render_depth_device
+from .render import tactile_image_obs_device
+from .tactile import device_taxels, force_field_device
+from .transforms import quat_conj, quat_mul, quat_rotate_inv
+
+PEG = 1  # body index of the peg (envs/peg_tasks.py:38: EE, PEG, SOCKET, TABLE)
+N_SENSORS = 2
+
+
+class _EnvDevice:
+    def __init__(self, env):
+        t = _device.torch()
+        c = env.cfg
+        self.device = _device.resolve_device(None)
+        self.E = int(env.num_envs)
+        W, H = (int(v) for v in c.tactile_image_size)
+        self.H, self.W = H, W
+        self.rays = RayTable(env.camera, env.background, self.device)
+        self.depth = t.empty((self.E, N_SENSORS, H, W), dtype=t.float32, device=self.device)
+        self.rgb = t.empty((self.E, N_SENSORS, H, W, 3), dtype=t.float32, device=self.device)
+        R, C = (int(v) for v in c.tactile_ff_grid)
+        self.R, self.C = R, C
+        self.taxels = device_taxels(env.ff_grid, self.device)
+        self.ff = t.empty((self.E, N_SENSORS, R, C, 3), dtype=t.float32, device=self.device)
+        self.key = (self.E, H, W, R, C)
+
+
+def _state(env) -> _EnvDevice:
+    c = env.cfg
+    key = (int(env.num_envs), int(c.tactile_image_size[1]), int(c.tactile_image_size[0]),
+           int(c.tactile_ff_grid[0]), int(c.tactile_ff_grid[1]))
+    st = getattr(env, "_tacsl", None)
+    if st is None or st.key != key:
+        st = _EnvDevice(env)
+        env._tacsl = st
+    return st
+
+
+def _relative_peg_poses(env):
+    """(E, 2, 3) / (E, 2, 4) peg pose in each finger's sensor frame, in the
+    reference's operation order (peg_tasks.py:440-442)."""
+    pos, quat = [], []
+    for s in range(N_SENSORS):
+        p, q = env._sensor_world_pose(s)
+        pos.append(quat_rotate_inv(q, env.bodies.pos[:, PEG] - p))
+        quat.append(quat_mul(quat_conj(q), env.bodies.quat[:, PEG]))
+    return np.stack(pos, axis=1), np.stack(quat, axis=1)
+
+
+def tactile_images(env) -> np.ndarray:
+    """PegEnvBatch._tactile_images for all envs and both fingers:
+    (E, 2, H, W, 3) float32 ("color" / "diff") or (E, 2, H, W, 6) ("concat")."""
+    t = _device.torch()
+    c = env.cfg
+    st = _state(env)
+    E = st.E
+    rel_pos, rel_quat = _relative_peg_poses(env)
+    params = _device.to_device(env_params(env.peg_sdf, rel_pos.reshape(-1, 3), rel_quat.reshape(-1, 4)),
+                               t.float64, st.device)
+    render_depth_device(st.rays, env.peg_sdf, params, out_f32=st.depth)
+    rep = c.tactile_rep
+    if c.augment is None:
+        out = tactile_image_obs_device(st.depth, env.lut, rep)
+    else:
+        seeds = (np.asarray(env.env_seeds, dtype=np.int64) * 1000003 + np.asarray(env.episode, dtype=np.int64))
+        steps = np.asarray(env.step_count, dtype=np.int64)
+        tactile_image_obs_device(st.depth, env.lut, "color", out=st.rgb)
+        nominal = np.asarray(env.lut.coeffs, dtype=np.float64)[:, 0].astype(np.float32)
+        out = augment_device(st.rgb, c.augment, np.repeat(seeds, N_SENSORS), np.repeat(steps, N_SENSORS),
+                             tactile_rep=rep, nominal=nominal)
+    return out.cpu().numpy().reshape((E, N_SENSORS) + tuple(out.shape[2:]))
+
+
+def tactile_ff(env) -> np.ndarray:
+    """PegEnvBatch._tactile_ff: (E, 2, R, C, 3) float32 = [f_n.z, f_t.x, f_t.y]
+    of each finger's force field in its sensor frame."""
+    t = _device.torch()
+    c = env.cfg
+    st = _state(env)
+    b = env.bodies
+    obj = np.concatenate([b.pos[:, PEG], b.quat[:, PEG], b.linvel[:, PEG], b.angvel[:, PEG]], axis=1)
+    sen = []
+    for s in range(N_SENSORS):
+        p, q = env._sensor_world_pose(s)
+        v, w = env._sensor_world_velocity(p)
+        sen.append(np.concatenate([p, q, v, w], axis=1))
+    sen = np.stack(sen, axis=1)
+    force_field_device(env.peg_sdf, st.taxels, st.R, st.C, _device.to_device(obj, t.float64, st.device),
+                       _device.to_device(np.ascontiguousarray(sen), t.float64, st.device), c.penalty,
+                       obs=st.ff, n_sensors=N_SENSORS, obj_stride=13, sen_stride=13 * N_SENSORS, n_envs=st.E)
+    return st.ff.cpu().numpy()

@@ -10,6 +10,9 @@ the defining one:
     gelsim.envs.peg_tasks, gelsim.envs.scenes depth_to_rgb, compute_force_field
     gelsim.geometry, gelsim.geometry.sdf      query_sdf (standalone API only)
 
+and replaces ``PegEnvBatch._tactile_images`` / ``_tactile_ff``
+(envs/peg_tasks.py:434-477) by their batched versions in ``envs.py``.
+
 ``query_sdf`` is deliberately NOT rebound at the physics call sites
 (physics/contacts.py:15, envs/peg_tasks.py _fit_grip): those are tiny CPU
 queries where a device round trip would only add latency; inside
@@ -33,6 +36,12 @@ _SITES = {
     "gelsim.geometry": ("query_sdf",),
 }
 
+# env methods replaced by their batched versions (envs.py): one launch per
+# kernel for both fingers of all envs instead of per-finger / per-env loops
+_METHODS = {
+    ("gelsim.envs.peg_tasks", "PegEnvBatch"): ("_tactile_images", "_tactile_ff"),
+}
+
 _saved: dict = {}
 
 
@@ -52,10 +61,30 @@ def _impl(name):
     }[name]
 
 
-def patch(modules=None) -> list:
-    """Rebind the hot-path names in every importable reference module.
-    Returns the list of (module, name) pairs rebound."""
+def _method_impl(name):
+    from . import envs
+
+    return {"_tactile_images": envs.tactile_images, "_tactile_ff": envs.tactile_ff}[name]
+
+
+def patch(modules=None, env_methods: bool = True) -> list:
+    """Rebind the hot-path names in every importable reference module (and,
+    with ``env_methods``, the env's tactile observation methods).  Returns the
+    list of (module, name) pairs rebound."""
     done = []
+    if env_methods:
+        for (mod_name, cls_name), names in _METHODS.items():
+            if modules is not None and mod_name not in modules:
+                continue
+            try:
+                cls = getattr(importlib.import_module(mod_name), cls_name)
+            except Exception:  # noqa: BLE001 - module absent in this install
+                continue
+            for n in names:
+                if n in cls.__dict__:
+                    _saved.setdefault((mod_name, f"{cls_name}.{n}"), cls.__dict__[n])
+                    setattr(cls, n, _method_impl(n))
+                    done.append((mod_name, f"{cls_name}.{n}"))
     for mod_name, names in _SITES.items():
         if modules is not None and mod_name not in modules:
             continue
@@ -73,6 +102,9 @@ def patch(modules=None) -> list:
 
 def unpatch() -> None:
     for (mod_name, n), fn in list(_saved.items()):
-        mod = importlib.import_module(mod_name)
-        setattr(mod, n, fn)
+        target = importlib.import_module(mod_name)
+        if "." in n:  # Class.method
+            cls_name, n = n.split(".", 1)
+            target = getattr(target, cls_name)
+        setattr(target, n, fn)
     _saved.clear()

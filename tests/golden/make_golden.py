@@ -294,7 +294,8 @@ def make_env():
         rel_pos=np.stack(rel_p, axis=1), rel_quat=np.stack(rel_q, axis=1), background=env.background,
         cam_dirs=env.camera.rays(),
         sen=np.stack(sen, axis=1), seeds=(env.env_seeds * 1000003 + env.episode).astype(np.int64),
-        steps=env.step_count.astype(np.int64), lut_coeffs=env.lut.coeffs, lut_degree=env.lut.degree,
+        steps=env.step_count.astype(np.int64), env_seeds=env.env_seeds.astype(np.int64),
+        episode=env.episode.astype(np.int64), lut_coeffs=env.lut.coeffs, lut_degree=env.lut.degree,
         image_size=np.array(cfg.tactile_image_size), ff_points=env.ff_grid.points,
         penalty=np.array([p.k_n, p.k_d, p.k_t, p.mu]),
         sdf_origin=np.asarray(g.origin), sdf_spacing=np.float64(g.spacing), sdf_dims=np.array(g.dims),

@@ -99,3 +99,55 @@ def test_shape_sensing_scene_end_to_end(golden_grid):
     assert np.array_equal(np.linalg.norm(fld.f_n, axis=-1) > 0, np.linalg.norm(z["f_n"], axis=-1) > 0)
     assert vec_close(fld.f_n, z["f_n"], 1e-5)[0]
     assert vec_close(fld.f_t, z["f_t"], 1e-5)[0]
+
+
+def _standin_env(env, aug_cfg):
+    """An object with exactly the attributes PegEnvBatch._tactile_images /
+    _tactile_ff read, filled from the recorded reference env."""
+    from types import SimpleNamespace
+
+    from paper_2408_06506_b200.envs import PEG
+    E = env["obj"].shape[0]
+    W, H = (int(v) for v in env["image_size"])
+    spec = TactileSensorSpec(image_size=(W, H))
+    cam = camera_for_sensor(spec)
+    bodies = SimpleNamespace(pos=np.zeros((E, 4, 3)), quat=np.zeros((E, 4, 4)), linvel=np.zeros((E, 4, 3)),
+                             angvel=np.zeros((E, 4, 3)))
+    bodies.pos[:, PEG], bodies.quat[:, PEG] = env["obj"][:, 0:3], env["obj"][:, 3:7]
+    bodies.linvel[:, PEG], bodies.angvel[:, PEG] = env["obj"][:, 7:10], env["obj"][:, 10:13]
+    pts = env["ff_points"]
+    grid = TactilePointGrid(points=pts, rest_normals=np.broadcast_to([0.0, 0.0, 1.0], pts.shape).copy(),
+                            spacing=(1.0, 1.0))
+    sen = env["sen"]
+    cfg = SimpleNamespace(tactile_image_size=(W, H), tactile_ff_grid=pts.shape[:2], tactile_rep="diff",
+                          augment=aug_cfg, penalty=PenaltyParams(*env["penalty"]))
+    return SimpleNamespace(
+        cfg=cfg, num_envs=E, camera=cam, background=reference_depth(cam, spec), peg_sdf=env["sdf"],
+        lut=env["lut"], env_seeds=env["env_seeds"], episode=env["episode"], step_count=env["steps"],
+        bodies=bodies, ff_grid=grid,
+        _sensor_world_pose=lambda s: (sen[:, s, 0:3], sen[:, s, 3:7]),
+        _sensor_world_velocity=lambda p: next((sen[:, s, 7:10], sen[:, s, 10:13]) for s in range(2)
+                                              if np.array_equal(p, sen[:, s, 0:3])))
+
+
+def test_batched_env_methods_reproduce_the_env(env):
+    """envs.tactile_images / tactile_ff (what patch() binds as
+    PegEnvBatch._tactile_images / _tactile_ff) on an object carrying the
+    recorded env's state reproduce the env's own observations."""
+    from paper_2408_06506_b200 import envs
+    a = env["aug"]
+    cfg = AugmentConfig(shift_px=a[0], zoom=(a[1], a[2]), brightness=a[3], contrast=(a[4], a[5]),
+                        saturation=(a[6], a[7]), hue=a[8], channel_permutation=bool(a[9]), step_brightness=a[10],
+                        step_contrast=(a[11], a[12]), step_saturation=(a[13], a[14]), step_hue=a[15],
+                        seed=int(a[16]))
+    e = _standin_env(env, cfg)
+    images = envs.tactile_images(e)
+    assert images.dtype == np.float32 and images.shape == env["images"].shape
+    diff = np.abs(images - env["images"])
+    assert diff.max() <= 1.0 / 255.0 and (diff > 1e-5).mean() < 0.01
+    ff = envs.tactile_ff(e)
+    assert ff.dtype == np.float32 and ff.shape == env["ff"].shape
+    assert np.array_equal(np.abs(ff).sum(-1) > 0, np.abs(env["ff"]).sum(-1) > 0)
+    assert vec_close(ff, env["ff"], 1e-5, atol=1e-7)[0]
+    # second step reuses the cached device state
+    assert np.array_equal(envs.tactile_images(e), images)

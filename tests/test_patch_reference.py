@@ -44,9 +44,13 @@ def test_patch_rebinds_and_unpatch_restores(gelsim):
     from paper_2408_06506_b200.augment import augment as augment_fn
     before = {(m, n): getattr(importlib.import_module(m), n)
               for m, names in patching._SITES.items() for n in names}
+    cls = importlib.import_module("gelsim.envs.peg_tasks").PegEnvBatch
+    methods = {n: cls.__dict__[n] for n in ("_tactile_images", "_tactile_ff")}
     done = patching.patch()
     try:
-        assert len(done) == len(before)
+        assert len(done) == len(before) + len(methods)
+        from paper_2408_06506_b200 import envs
+        assert cls._tactile_images is envs.tactile_images and cls._tactile_ff is envs.tactile_ff
         peg = importlib.import_module("gelsim.envs.peg_tasks")
         assert peg.depth_to_rgb is render.depth_to_rgb
         assert peg.compute_force_field is tactile.compute_force_field
@@ -61,6 +65,8 @@ def test_patch_rebinds_and_unpatch_restores(gelsim):
         patching.unpatch()
     for (m, n), fn in before.items():
         assert getattr(importlib.import_module(m), n) is fn
+    for n, fn in methods.items():
+        assert cls.__dict__[n] is fn
 
 
 def test_reference_exceptions_are_reexported(gelsim):

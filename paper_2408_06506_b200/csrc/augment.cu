@@ -258,68 +258,75 @@ __device__ __forceinline__ void apply_color(float v[3], double b, double c, doub
   }
 }
 
+// Grid: x strides over an image's pixels, y over images, so the per-image
+// parameters and the branches they select are uniform across a CTA and no
+// 64-bit division is needed per pixel.
 __global__ void __launch_bounds__(256) augment_apply_kernel(const float* __restrict__ in, int64_t n, int H, int W,
                                                             const double* __restrict__ params, int rep, float n0,
                                                             float n1, float n2, float* __restrict__ out) {
-  const int64_t total = n * (int64_t)H * W;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int HW = H * W;
   const float hc = (float)((H - 1) / 2.0), wc = (float)((W - 1) / 2.0);
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int64_t img = idx / ((int64_t)H * W);
-    const int rem = (int)(idx - img * (int64_t)H * W);
-    const int y = rem / W, x = rem - y * W;
+  for (int64_t img = blockIdx.y; img < n; img += gridDim.y) {
     const double* P = params + img * 16;
-    const float* src = in + img * (int64_t)H * W * 3;
-    float v[3];
+    const float* src = in + img * (int64_t)HW * 3;
     const double zoom = P[P_ZOOM], sx = P[P_SX], sy = P[P_SY];
-    if (zoom != 1.0 || sx != 0.0 || sy != 0.0) {
-      // _resample_bilinear (augment.py:121-140)
-      const float zf = (float)zoom;
-      const float izf = __frcp_rn(zf);
-      float ys = fsub(fadd(div_y(fsub((float)y, hc), zf, izf), hc), (float)sy);
-      float xs = fsub(fadd(div_y(fsub((float)x, wc), zf, izf), wc), (float)sx);
-      ys = fminf(fmaxf(ys, 0.f), (float)(H - 1));
-      xs = fminf(fmaxf(xs, 0.f), (float)(W - 1));
-      const int y0 = min(max((int)ys, 0), H - 2), x0 = min(max((int)xs, 0), W - 2);
-      const float fy = fsub(ys, (float)y0), fx = fsub(xs, (float)x0);
-      const float ufx = fsub(1.f, fx), ufy = fsub(1.f, fy);
-      const float* a = src + ((size_t)y0 * W + x0) * 3;
-      const float* c = a + (size_t)W * 3;
-      for (int k = 0; k < 3; ++k) {
-        const float top = fadd(fmul(a[k], ufx), fmul(a[3 + k], fx));
-        const float bot = fadd(fmul(c[k], ufx), fmul(c[3 + k], fx));
-        v[k] = fadd(fmul(top, ufy), fmul(bot, fy));
-      }
-    } else {
-      const float* a = src + (size_t)rem * 3;
-      v[0] = a[0];
-      v[1] = a[1];
-      v[2] = a[2];
-    }
+    const bool resample = zoom != 1.0 || sx != 0.0 || sy != 0.0;
+    const float zf = (float)zoom, izf = __frcp_rn(zf), sxf = (float)sx, syf = (float)sy;
     const int p0 = (int)P[P_P0], p1 = (int)P[P_P1], p2 = (int)P[P_P2];
-    if (p0 != 0 || p1 != 1 || p2 != 2) {
-      const float w0 = v[p0], w1 = v[p1], w2 = v[p2];
-      v[0] = w0;
-      v[1] = w1;
-      v[2] = w2;
-    }
-    apply_color(v, P[P_B], P[P_C], P[P_S], P[P_H]);
+    const bool permute = p0 != 0 || p1 != 1 || p2 != 2;
+    const double b = P[P_B], c = P[P_C], sat = P[P_S], hue = P[P_H];
     const double db = P[P_DB], dc = P[P_DC], ds = P[P_DS], dh = P[P_DH];
-    if (db != 0.0 || dc != 1.0 || ds != 1.0 || dh != 0.0) apply_color(v, db, dc, ds, dh);
-    for (int k = 0; k < 3; ++k) v[k] = clip01(v[k]);
-    if (rep == 2) {
-      float* o = out + idx * 6;
-      o[0] = v[0];
-      o[1] = v[1];
-      o[2] = v[2];
-      o[3] = n0;
-      o[4] = n1;
-      o[5] = n2;
-    } else {
-      float* o = out + idx * 3;
-      o[0] = rep == 1 ? fsub(v[0], n0) : v[0];
-      o[1] = rep == 1 ? fsub(v[1], n1) : v[1];
-      o[2] = rep == 1 ? fsub(v[2], n2) : v[2];
+    const bool step_jitter = db != 0.0 || dc != 1.0 || ds != 1.0 || dh != 0.0;
+    for (int rem = blockIdx.x * blockDim.x + threadIdx.x; rem < HW; rem += gridDim.x * blockDim.x) {
+      const int y = rem / W, x = rem - y * W;
+      float v[3];
+      if (resample) {
+        // _resample_bilinear (augment.py:121-140)
+        float ys = fsub(fadd(div_y(fsub((float)y, hc), zf, izf), hc), syf);
+        float xs = fsub(fadd(div_y(fsub((float)x, wc), zf, izf), wc), sxf);
+        ys = fminf(fmaxf(ys, 0.f), (float)(H - 1));
+        xs = fminf(fmaxf(xs, 0.f), (float)(W - 1));
+        const int y0 = min(max((int)ys, 0), H - 2), x0 = min(max((int)xs, 0), W - 2);
+        const float fy = fsub(ys, (float)y0), fx = fsub(xs, (float)x0);
+        const float ufx = fsub(1.f, fx), ufy = fsub(1.f, fy);
+        const float* a = src + ((size_t)y0 * W + x0) * 3;
+        const float* cc = a + (size_t)W * 3;
+        for (int k = 0; k < 3; ++k) {
+          const float top = fadd(fmul(a[k], ufx), fmul(a[3 + k], fx));
+          const float bot = fadd(fmul(cc[k], ufx), fmul(cc[3 + k], fx));
+          v[k] = fadd(fmul(top, ufy), fmul(bot, fy));
+        }
+      } else {
+        const float* a = src + (size_t)rem * 3;
+        v[0] = a[0];
+        v[1] = a[1];
+        v[2] = a[2];
+      }
+      if (permute) {  // selects, not a dynamically indexed (local-memory) array
+        auto pick = [&](int k) { return k == 0 ? v[0] : (k == 1 ? v[1] : v[2]); };
+        const float w0 = pick(p0), w1 = pick(p1), w2 = pick(p2);
+        v[0] = w0;
+        v[1] = w1;
+        v[2] = w2;
+      }
+      apply_color(v, b, c, sat, hue);
+      if (step_jitter) apply_color(v, db, dc, ds, dh);
+      for (int k = 0; k < 3; ++k) v[k] = clip01(v[k]);
+      const int64_t idx = img * (int64_t)HW + rem;
+      if (rep == 2) {
+        float* o = out + idx * 6;
+        o[0] = v[0];
+        o[1] = v[1];
+        o[2] = v[2];
+        o[3] = n0;
+        o[4] = n1;
+        o[5] = n2;
+      } else {
+        float* o = out + idx * 3;
+        o[0] = rep == 1 ? fsub(v[0], n0) : v[0];
+        o[1] = rep == 1 ? fsub(v[1], n1) : v[1];
+        o[2] = rep == 1 ? fsub(v[2], n2) : v[2];
+      }
     }
   }
 }
@@ -350,9 +357,12 @@ extern "C" int tacsl_augment(const float* images, int64_t n, int height, int wid
   if (!images || !params || !out || (rep && !nominal))
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: null pointer");
   if (images == out) return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: in-place is not supported");
-  const int64_t total = n * (int64_t)height * width;
+  const int64_t hw = (int64_t)height * width;
+  const int64_t total = n * hw;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(current_device()) * 16);
-  augment_apply_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+  const unsigned gy = (unsigned)std::min<int64_t>(n, 65535);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((hw + 255) / 256, (blocks + gy - 1) / gy));
+  augment_apply_kernel<<<dim3(gx, gy), 256, 0, (cudaStream_t)stream>>>(
       images, n, height, width, params, rep, rep ? nominal[0] : 0.f, rep ? nominal[1] : 0.f,
       rep ? nominal[2] : 0.f, out);
   return check_launch("augment_apply_kernel");

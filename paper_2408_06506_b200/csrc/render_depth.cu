@@ -48,11 +48,10 @@ __global__ void __launch_bounds__(256) render_depth_kernel(const RenderParams P,
                                                            const double* __restrict__ background,
                                                            const double* __restrict__ envp, int64_t n_envs,
                                                            double* __restrict__ out64, float* __restrict__ out32) {
-  const int64_t total = n_envs * (int64_t)P.n_rays;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int64_t e = idx / P.n_rays;
-    const int r = (int)(idx - e * P.n_rays);
+  // grid: y over envs, x over an env's rays (no 64-bit division per ray)
+  for (int64_t e = blockIdx.y; e < n_envs; e += gridDim.y)
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n_rays; r += gridDim.x * blockDim.x) {
+    const int64_t idx = e * P.n_rays + r;
     const double* ep = envp + e * 18;  // pos[3], rot[9] (object->sensor, row-major), lo[3], hi[3]
     const double dx = __ldg(dirs + 3 * r), dy = __ldg(dirs + 3 * r + 1), dz = __ldg(dirs + 3 * r + 2);
     const double bg = __ldg(background + r);
@@ -166,7 +165,10 @@ extern "C" int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const dou
   P.n_rays = height * width;
   const int64_t total = n_envs * (int64_t)P.n_rays;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(current_device()) * 32);
-  render_depth_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(P, dirs, background, env_params, n_envs,
-                                                                          depth_f64, depth_f32);
+  const unsigned gy = (unsigned)std::min<int64_t>(n_envs, 65535);
+  const unsigned gx = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((P.n_rays + 255) / 256, (blocks + gy - 1) / gy));
+  render_depth_kernel<<<dim3(gx, gy), 256, 0, (cudaStream_t)stream>>>(P, dirs, background, env_params, n_envs,
+                                                                      depth_f64, depth_f32);
   return check_launch("render_depth_kernel");
 }

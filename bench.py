@@ -453,10 +453,18 @@ def main():
         fpc = max(1, min(int(args.cpu_seconds / max(per_core_frame, 1e-3)), wl.frames // base.cores))
         n, dt = base.run(fpc)
         base.close()
+        # the 1-process figure beside it: one single-threaded worker
+        one = CpuBaseline(wl, cores=1)
+        n1, t1 = one.run(1)
+        k1 = max(1, min(int(3.0 / max(t1, 1e-3)), 64))
+        n1, t1 = one.run(k1)
+        one.close()
         line["cpu_baseline"] = {
             "value": n / dt, "unit": UNIT, "cores": base.cores, "kind": "port",
             "sample": f"{n} sensor frames of config {wl.config_id} ({fpc} per core), numpy oracle "
                       f"restating gelsim depth_to_rgb+to_uint8+compute_force_field+net_wrench; {cpu_model()}",
+            "single_process": {"value": n1 / t1, "unit": UNIT, "cores": 1,
+                               "sample": f"{n1} sensor frames on one single-threaded worker"},
         }
     if rank == 0:
         print(json.dumps(line), flush=True)

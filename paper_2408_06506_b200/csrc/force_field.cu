@@ -67,11 +67,11 @@ __global__ void __launch_bounds__(128, MINB) force_field_kernel(const FFArgs<Out
 // shared memory; per taxel 9 FMAs give the cell coordinates, trilinear
 // lerps the distance, and only taxels the fast values cannot decide replay
 // the exact chain.  Used whenever kinematics are not requested.
-template <typename OutT, int MINB>
-__global__ void __launch_bounds__(128, MINB) force_field_fast_kernel(const FFArgs<OutT> A) {
+template <typename OutT, int MINB, int MAXT = 128>
+__global__ void __launch_bounds__(MAXT, MINB) force_field_fast_kernel(const FFArgs<OutT> A) {
   const int64_t frame = blockIdx.x;
   __shared__ FrameC C;
-  __shared__ double part[8][6];
+  __shared__ double part[MAXT / 32][6];
   if (threadIdx.x < 32) frame_setup_warp(A, frame, C, threadIdx.x);
   __syncthreads();
   const Grid& g = A.grid;
@@ -317,7 +317,9 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
   // threads per frame: small taxel grids (20x25) amortise the per-frame
   // set-up best with 2 warps per frame, dense ones (80x100) with 4 (measured)
   const char* tpf = std::getenv("TACSL_FF_THREADS");
-  const int threads = tpf ? (std::atoi(tpf) == 64 ? 64 : 128) : (n_taxels <= 1024 ? 64 : 128);
+  // (and a small batch -- fewer frames than SMs -- wants the wider CTA for latency)
+  const bool few = frames < 2 * (int64_t)sm_count(current_device());
+  const int threads = tpf ? (std::atoi(tpf) == 64 ? 64 : 128) : (n_taxels <= 1024 && !few ? 64 : 128);
   Penalty P{params.k_n, params.k_d, params.k_t, params.mu};
   cudaStream_t s = (cudaStream_t)stream;
   const char* mb = std::getenv("TACSL_FF_MINBLOCKS");
@@ -330,7 +332,10 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
     using O = decltype(out_tag);
     const FFArgs<O> A{make_grid(sdf), taxels, n_taxels, object_state, object_stride, sensor_state, sensor_stride,
                       n_sensors, frames, P, (O*)f_n, (O*)f_t, wrench, kin, contact, obs};
-    if (!kin && !exact) {
+    if (!kin && !exact && few && n_taxels >= 256 && !tpf) {
+      // a handful of frames: one taxel (or two) per thread, lowest latency
+      force_field_fast_kernel<O, 1, 512><<<(unsigned)frames, std::min(512, (n_taxels + 31) / 32 * 32), 0, s>>>(A);
+    } else if (!kin && !exact) {
       if (minb_fast >= 6) force_field_fast_kernel<O, 6><<<(unsigned)frames, threads, 0, s>>>(A);
       else if (minb_fast == 5) force_field_fast_kernel<O, 5><<<(unsigned)frames, threads, 0, s>>>(A);
       else force_field_fast_kernel<O, 4><<<(unsigned)frames, threads, 0, s>>>(A);

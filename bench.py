@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--no-overlap", action="store_true")
     p.add_argument("--fused", action="store_true", help="one launch (force-field warps inside K1) per step")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     p.add_argument("--e2e-chunks", type=int, default=64, help="env chunks pipelined over H2D / compute / D2H")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample length")
@@ -354,30 +354,37 @@ def main():
             if host[k] is not None:
                 host[k].copy_(v)
 
-        def e2e_step():
-            arr.run_host(host, depth, obj, sen, chunks=args.e2e_chunks)
+        if use_graph:  # the whole pipelined host-to-host step as one graph (SensorArray.capture_host)
+            arr.capture_host(host, depth, obj, sen, chunks=args.e2e_chunks)
+            e2e_step = arr.replay_host
+        else:
+            def e2e_step():
+                arr.run_host(host, depth, obj, sen, chunks=args.e2e_chunks)
 
         for _ in range(2):  # warm: first-touch of the pinned pages, stream / event pools
             e2e_step()
         torch.cuda.synchronize()
         barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.e2e_steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps + 1)]
+        ev[0].record(stream)
+        for i in range(args.e2e_steps):
             e2e_step()
-        b.record(stream)
+            ev[i + 1].record(stream)
         torch.cuda.synchronize()
         barrier()
-        ms = max_over_ranks(a.elapsed_time(b)) / args.e2e_steps
+        per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.e2e_steps)]
+        ms = max_over_ranks(ev[0].elapsed_time(ev[-1])) / args.e2e_steps
         h2d = sum(host[k].numel() * host[k].element_size() for k in ("depth", "obj", "sen")
                   if host[k] is not None) * world
         d2h = sum(v.numel() * v.element_size() for k, v in host.items()
                   if v is not None and k not in ("depth", "obj", "sen")) * world
         return {"value": frames_total / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
-                "api": "SensorArray.run_host: pinned host depth+states in, pinned host RGB+forces+wrench out, "
-                       f"{args.e2e_chunks} env chunks pipelined over H2D / kernels / D2H streams"}
+                "step_ms_min_median_max": [min(per_step), float(np.median(per_step)), max(per_step)],
+                "api": ("SensorArray.capture_host/replay_host" if use_graph else "SensorArray.run_host")
+                       + ": pinned host depth+states in, pinned host RGB+forces+wrench out, "
+                       f"{args.e2e_chunks} env chunks pipelined over H2D / kernels / D2H streams"
+                       + (", one CUDA graph per step" if use_graph else "")}
 
     e2e = None if args.no_e2e else measure_e2e()
 

@@ -236,6 +236,27 @@ class SensorArray:
         main.wait_stream(self._d2h)
         return host
 
+    def capture_host(self, host, depth, obj_state, sen_state, chunks=8):
+        """Record run_host(...) -- every chunk's copies and kernels on the
+        three streams -- as one CUDA graph bound to these host and device
+        buffers; replay_host() then runs a whole host-to-host step with one
+        launch and no per-chunk host work."""
+        t = _device.torch()
+        s = t.cuda.Stream(device=self.device)
+        s.wait_stream(t.cuda.current_stream(self.device))
+        with t.cuda.stream(s):
+            self.run_host(host, depth, obj_state, sen_state, chunks)  # warm-up outside capture
+        t.cuda.current_stream(self.device).wait_stream(s)
+        t.cuda.synchronize(self.device)
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g):
+            self.run_host(host, depth, obj_state, sen_state, chunks)
+        self._host_graph = g
+        return g
+
+    def replay_host(self):
+        self._host_graph.replay()
+
 
 class TactileObservations:
     """Batched tactile observations of the 2-finger peg env: the outputs of

@@ -13,9 +13,14 @@ def torch():
     return _t
 
 
+_checked: dict = {}  # device index -> supported; availability checked once per process
+
+
 def resolve_device(device=None):
     t = torch()
-    if not t.cuda.is_available():
+    if "available" not in _checked:  # torch.cuda.is_available() can cost tens of ms per call
+        _checked["available"] = t.cuda.is_available()
+    if not _checked["available"]:
         raise RuntimeError(
             "paper_2408_06506_b200 runs on a CUDA B200 (sm_100a) device only; "
             "torch.cuda.is_available() is False and there is no CPU fallback")
@@ -27,8 +32,10 @@ def resolve_device(device=None):
             raise RuntimeError(f"device {dev} is not a CUDA device; there is no CPU fallback")
         if dev.index is None:
             dev = t.device("cuda", t.cuda.current_device())
-    lib = _lib.load()
-    if not lib.tacsl_device_supported(dev.index):
+    ok = _checked.get(dev.index)
+    if ok is None:
+        ok = _checked[dev.index] = bool(_lib.load().tacsl_device_supported(dev.index))
+    if not ok:
         raise RuntimeError(f"cuda:{dev.index} is not an sm_100 (B200) GPU; libtacsl_b200 has sm_100a code only")
     return dev
 

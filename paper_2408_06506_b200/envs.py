@@ -73,7 +73,16 @@ def _relative_peg_poses(env):
 
 def tactile_images(env) -> np.ndarray:
     """PegEnvBatch._tactile_images for all envs and both fingers:
-    (E, 2, H, W, 3) float32 ("color" / "diff") or (E, 2, H, W, 6) ("concat")."""
+    (E, 2, H, W, 3) float32 ("color" / "diff") or (E, 2, H, W, 6) ("concat"),
+    as a fresh numpy array like the reference's (at 4096 envs that host copy
+    -- 0.47 GB -- dominates; GPU-resident consumers use
+    ``tactile_images_device``)."""
+    return tactile_images_device(env).cpu().numpy()
+
+
+def tactile_images_device(env):
+    """tactile_images as a CUDA tensor (E, 2, H, W, C) float32 -- a buffer
+    owned by the env's device state, valid until the next call."""
     t = _device.torch()
     c = env.cfg
     st = _state(env)
@@ -92,12 +101,17 @@ def tactile_images(env) -> np.ndarray:
         nominal = np.asarray(env.lut.coeffs, dtype=np.float64)[:, 0].astype(np.float32)
         out = augment_device(st.rgb, c.augment, np.repeat(seeds, N_SENSORS), np.repeat(steps, N_SENSORS),
                              tactile_rep=rep, nominal=nominal)
-    return out.cpu().numpy().reshape((E, N_SENSORS) + tuple(out.shape[2:]))
+    return out.reshape((E, N_SENSORS) + tuple(out.shape[2:]))
 
 
 def tactile_ff(env) -> np.ndarray:
     """PegEnvBatch._tactile_ff: (E, 2, R, C, 3) float32 = [f_n.z, f_t.x, f_t.y]
-    of each finger's force field in its sensor frame."""
+    of each finger's force field in its sensor frame (fresh numpy array)."""
+    return tactile_ff_device(env).cpu().numpy()
+
+
+def tactile_ff_device(env):
+    """tactile_ff as a CUDA tensor, valid until the next call."""
     t = _device.torch()
     c = env.cfg
     st = _state(env)
@@ -112,4 +126,4 @@ def tactile_ff(env) -> np.ndarray:
     force_field_device(env.peg_sdf, st.taxels, st.R, st.C, _device.to_device(obj, t.float64, st.device),
                        _device.to_device(np.ascontiguousarray(sen), t.float64, st.device), c.penalty,
                        obs=st.ff, n_sensors=N_SENSORS, obj_stride=13, sen_stride=13 * N_SENSORS, n_envs=st.E)
-    return st.ff.cpu().numpy()
+    return st.ff

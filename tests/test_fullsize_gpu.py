@@ -109,7 +109,9 @@ def test_full_batch_frames_are_independent(full):
     torch.cuda.synchronize()
     assert torch.equal(f_n, arr.f_n[env])
     assert torch.equal(f_t, arr.f_t[env])
-    assert torch.equal(w, arr.wrench[env])
+    # a small batch runs wider CTAs per frame, so the per-sensor fp64 sum is
+    # reduced in a different order: equal to rounding, not bit for bit
+    torch.testing.assert_close(w, arr.wrench[env], rtol=1e-12, atol=1e-15)
 
 
 @pytest.mark.parametrize("axis,k", [(-1, 1), (-1, 4), (-1, 37), (-2, 1), (-2, 8), (-2, 61)])

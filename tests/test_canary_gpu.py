@@ -90,3 +90,25 @@ def test_k2_canaries(grid, E, S):
     torch.cuda.synchronize()
     assert all(intact(f, dt) for f, dt in ((fa, torch.float32), (fb, torch.float32), (fc, torch.float64),
                                            (fd, torch.float32)))
+
+
+@pytest.mark.parametrize("size,E", [((80, 60), 3), ((37, 29), 5)])
+def test_k3_k4_canaries(size, E):
+    from paper_2408_06506_b200 import AugmentConfig
+    from paper_2408_06506_b200.augment import augment_device
+    from paper_2408_06506_b200.depth import RayTable, env_params, render_depth_device
+    W, H = size
+    _, cam, bg, lut, _ = synthetic.sensor_setup(size)
+    sdf = synthetic.peg_grid((32, 32, 64))
+    obj, _ = synthetic.peg_states(E, 1, config_id=6, random_sensor_pose=False)
+    params = torch.from_numpy(env_params(sdf, obj[:, 0:3], obj[:, 3:7])).cuda()
+    d64, f64 = guarded((E, H, W), torch.float64)
+    d32, f32 = guarded((E, H, W), torch.float32)
+    render_depth_device(RayTable(cam, bg, torch.device("cuda")), sdf, params, out_f64=d64, out_f32=d32)
+    rgb = torch.rand((E, H, W, 3), device="cuda")
+    cfg = AugmentConfig(shift_px=1.0, zoom=(0.9, 1.1), brightness=0.05, hue=0.02, channel_permutation=True, seed=3)
+    seeds = torch.arange(E, dtype=torch.int64, device="cuda")
+    out, fo = guarded((E, H, W, 6), torch.float32)
+    augment_device(rgb, cfg, seeds, seeds, tactile_rep="concat", nominal=np.float32([0.3, 0.4, 0.5]), out=out)
+    torch.cuda.synchronize()
+    assert intact(f64, torch.float64) and intact(f32, torch.float32) and intact(fo, torch.float32)

@@ -19,6 +19,10 @@ struct LutParams {
   float nominal[3];
 };
 
+// K6 on the K1 band pipeline (rgb.cu): coefficient pairs (c, c), (sets, 3, T)
+int launch_rgb_binned(const float2* pairs, int bins_y, int bins_x, int degree, const float* depth, int64_t n,
+                      int H, int W, uint8_t* u8, float* f32, cudaStream_t s);
+
 }  // namespace tacsl
 
 struct tacsl_lut_s {

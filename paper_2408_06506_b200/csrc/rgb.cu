@@ -25,6 +25,7 @@
 #include <array>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -86,6 +87,29 @@ __device__ __forceinline__ float2 poly2_sat(const float (&c)[15], float2 hx, flo
   return out;
 }
 
+// poly2_sat with per-thread coefficient PAIRS (c, c) read through L1 (the
+// binned LUT: each pixel pair's bin has its own table, K6)
+template <int DEG>
+__device__ __forceinline__ float2 poly2_sat_p(const float2* __restrict__ c, float2 hx, float2 hy) {
+  float2 acc = bc(0.f);
+  float2 out = bc(0.f);
+#pragma unroll
+  for (int i = DEG; i >= 0; --i) {
+    float2 p = __ldg(c + term_index(i, DEG - i));
+#pragma unroll
+    for (int j = DEG - i - 1; j >= 0; --j) p = __ffma2_rn(p, hy, __ldg(c + term_index(i, j)));
+    if (i == DEG) {
+      acc = p;
+    } else if (i > 0) {
+      acc = __ffma2_rn(acc, hx, p);
+    } else {
+      out.x = __saturatef(__fmaf_rn(acc.x, hx.x, p.x));
+      out.y = __saturatef(__fmaf_rn(acc.y, hx.y, p.y));
+    }
+  }
+  return out;
+}
+
 __device__ __forceinline__ uint32_t q8(float x) {
   // clip(rint(255 x), 0, 255): x is saturated to [0,1] first, then the
   // 1.5*2^23 bias rounds the exact product half-to-even into the low byte.
@@ -101,6 +125,13 @@ __device__ __forceinline__ void shade(const LutParams& L, float hx, float hy, fl
   g = __saturatef(poly<DEG>(L.c[1], hx, hy));
   b = __saturatef(poly<DEG>(L.c[2], hx, hy));
 }
+
+// Binned LUT (K6 on this pipeline): (bins_y * bins_x, 3, T) coefficient
+// pairs; the host guarantees no pixel pair straddles an x-bin edge.
+struct BinArgs {
+  const float2* __restrict__ pairs;
+  int bins_y, bins_x;
+};
 
 struct Layout {
   int band, rpt, groups, stages;
@@ -119,12 +150,13 @@ struct Layout {
 //   empty[s] : every consumer warp has its rows of stage s in registers
 //   ready[b] : every consumer warp wrote its part of output tile b
 //   ofree[b] : the bulk store of tile b has finished reading it
-template <int DEG, int RPT, bool U8, bool F32, bool FF>
+template <int DEG, int RPT, bool U8, bool F32, bool FF, bool BIN = false>
 __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMaxThreads + 64, 1) rgb_bulk_kernel(const float* __restrict__ depth,
                                                                     int64_t n_images, int H, int W, int groups,
                                                                     int stages, uint8_t* __restrict__ out_u8,
                                                                     float* __restrict__ out_f32, const LutParams L,
-                                                                    int bulk_store, const FFArgs<float> F) {
+                                                                    int bulk_store, const FFArgs<float> F,
+                                                                    const BinArgs B) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int QW = W >> 2;
   const int n_cons = QW * groups;
@@ -226,6 +258,8 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
   const int x0 = xq << 2;
   const bool at_left = (x0 == 0), at_right = (x0 + 4 >= W);
   const int loff = at_left ? 0 : -1, roff = at_right ? 3 : 4;
+  // binned LUT: x bins of the thread's two pixel pairs (fixed for the thread)
+  const int xba = BIN ? x0 * B.bins_x / W : 0, xbb = BIN ? (x0 + 2) * B.bins_x / W : 0;
   const float m0 = at_left ? 2.f : 1.f;  // np.gradient one-sided borders are not halved:
   const float m3 = at_right ? 2.f : 1.f; // h = 2*(f1-f0) in the doubled-gradient form
   const int lr0 = g * RPT;
@@ -253,6 +287,12 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
       uint32_t* op = reinterpret_cast<uint32_t*>(out_buf + (size_t)b * out_stage + row_off * 3);
       const int och = L.rep == 2 ? 6 : 3;  // float channels per output pixel
       float* of = F32 ? out_f32 + (((size_t)img * H + r0) * W + row_off) * och : nullptr;
+      constexpr int T = (DEG + 1) * (DEG + 2) / 2;
+      int yb = 0, ynext = 0;
+      if constexpr (BIN) {  // y bin of this thread's first row and the first row of the next bin
+        yb = (r0 + lr0) * B.bins_y / H;
+        ynext = ((yb + 1) * H + B.bins_y - 1) / B.bins_y;
+      }
       // a missing neighbour row / column is read as the pixel itself (the
       // offsets select it), so there is no select or copy in the row loop
       float4 c = *reinterpret_cast<const float4*>(p);
@@ -274,12 +314,28 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
         }
         const float2 hx01 = make_float2((c.y - left) * m0, c.z - c.x);
         const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
-        const float2 r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
-        const float2 g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
-        const float2 b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
-        const float2 r23 = poly2_sat<DEG>(L.c[0], hx23, hy23);
-        const float2 g23 = poly2_sat<DEG>(L.c[1], hx23, hy23);
-        const float2 b23 = poly2_sat<DEG>(L.c[2], hx23, hy23);
+        float2 r01, g01, b01, r23, g23, b23;
+        if constexpr (BIN) {
+          while (r >= ynext) {  // rows cross into the next y bin (at most once per row)
+            ++yb;
+            ynext = ((yb + 1) * H + B.bins_y - 1) / B.bins_y;
+          }
+          const float2* pa = B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T;
+          const float2* pb = B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T;
+          r01 = poly2_sat_p<DEG>(pa, hx01, hy01);
+          g01 = poly2_sat_p<DEG>(pa + T, hx01, hy01);
+          b01 = poly2_sat_p<DEG>(pa + 2 * T, hx01, hy01);
+          r23 = poly2_sat_p<DEG>(pb, hx23, hy23);
+          g23 = poly2_sat_p<DEG>(pb + T, hx23, hy23);
+          b23 = poly2_sat_p<DEG>(pb + 2 * T, hx23, hy23);
+        } else {
+          r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
+          g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
+          b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
+          r23 = poly2_sat<DEG>(L.c[0], hx23, hy23);
+          g23 = poly2_sat<DEG>(L.c[1], hx23, hy23);
+          b23 = poly2_sat<DEG>(L.c[2], hx23, hy23);
+        }
         if (U8) {
           // pixel order p0..p3, channel-interleaved: (r0 g0 b0 r1)(g1 b1 r2 g2)(b2 r3 g3 b3)
           const float2 qa = q8x2(make_float2(r01.x, g01.x));
@@ -423,10 +479,11 @@ int bulk_threads(int W, int groups, bool ff) {
   return (((W / 4) * groups + 31) / 32) * 32 + 64 + (ff ? kFFWarps * 32 : 0);
 }
 
-template <int DEG, int RPT, bool U8, bool F32, bool FF = false>
+template <int DEG, int RPT, bool U8, bool F32, bool FF = false, bool BIN = false>
 int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f32,
-                const LutParams& L, cudaStream_t stream, const FFArgs<float>* ff = nullptr) {
-  auto kern = rgb_bulk_kernel<DEG, RPT, U8, F32, FF>;
+                const LutParams& L, cudaStream_t stream, const FFArgs<float>* ff = nullptr,
+                const BinArgs* bin = nullptr) {
+  auto kern = rgb_bulk_kernel<DEG, RPT, U8, F32, FF, BIN>;
   static std::mutex mu;
   static std::vector<std::array<int, 4>> cache;  // (H, W, stages) -> groups
   const int QW = W / 4;
@@ -476,8 +533,10 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
   const int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
   FFArgs<float> F{};
   if (FF) F = *ff;
+  BinArgs B{};
+  if (BIN) B = *bin;
   kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
-                                                  bulk_store, F);
+                                                  bulk_store, F, B);
   return check_launch("rgb_bulk_kernel");
 }
 
@@ -505,6 +564,28 @@ int dispatch(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f3
 }
 
 }  // namespace
+
+// The binned LUT (K6) on this pipeline; called by binned.cu when the bin
+// edges fall between pixel pairs (even columns) and the layout is aligned.
+int launch_rgb_binned(const float2* pairs, int bins_y, int bins_x, int degree, const float* depth, int64_t n,
+                      int H, int W, uint8_t* u8, float* f32, cudaStream_t s) {
+  LutParams L{};  // rep 0 ("color") float epilogue; coefficients come from the table
+  const BinArgs B{pairs, bins_y, bins_x};
+  const Layout lay = base_layout(H, W, u8 != nullptr);
+  auto go = [&](auto deg) -> int {
+    constexpr int D = decltype(deg)::value;
+    if (u8 && f32) return launch_bulk<D, 8, true, true, false, true>(lay, depth, n, H, W, u8, f32, L, s, nullptr, &B);
+    if (u8) return launch_bulk<D, 8, true, false, false, true>(lay, depth, n, H, W, u8, f32, L, s, nullptr, &B);
+    return launch_bulk<D, 8, false, true, false, true>(lay, depth, n, H, W, u8, f32, L, s, nullptr, &B);
+  };
+  switch (degree) {
+    case 2: return go(std::integral_constant<int, 2>{});
+    case 3: return go(std::integral_constant<int, 3>{});
+    case 4: return go(std::integral_constant<int, 4>{});
+  }
+  return set_error(TACSL_ERR_INVALID_ARGUMENT, "LUT degree must be in [2, 4]");
+}
+
 }  // namespace tacsl
 
 using namespace tacsl;

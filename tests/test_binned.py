@@ -103,3 +103,27 @@ def test_gpu_binned_errors():
     big = BinnedPolyLut(degree=4, coeffs=np.zeros((60, 80, 3, 15)), image_size=(80, 60))
     with pytest.raises(ValueError):  # table larger than shared memory
         depth_to_rgb_binned(torch.from_numpy(d).cuda(), big)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bins", [(24, 32), (12, 40), (3, 80)])
+def test_gpu_band_pipeline_binned_equals_simple_kernel(monkeypatch, bins):
+    """Narrow bins run on K1's band pipeline (rgb_bulk_kernel<..., BIN>), wide
+    ones on the per-quad kernel: both evaluate the same FMA sequence per
+    pixel, so they agree bit for bit."""
+    import torch
+    from paper_2408_06506_b200.binned import depth_to_rgb_binned_device
+    size = (320, 240)
+    d, lut = _setup(size, n=6, cid=95)
+    lut = synthetic.synthetic_lut(size, degree=3, gradient_scale=synthetic.lut_scale(size))
+    v = vignetted_lut(lut, bins=bins, falloff=0.3)
+    dd = torch.from_numpy(d).cuda()
+    a = torch.empty(dd.shape + (3,), dtype=torch.uint8, device="cuda")
+    fa = torch.empty(dd.shape + (3,), dtype=torch.float32, device="cuda")
+    depth_to_rgb_binned_device(dd, v, out_u8=a, out_f32=fa)
+    monkeypatch.setenv("TACSL_BINNED_SIMPLE", "1")
+    b = torch.empty_like(a)
+    fb = torch.empty_like(fa)
+    depth_to_rgb_binned_device(dd, v, out_u8=b, out_f32=fb)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(fa, fb)

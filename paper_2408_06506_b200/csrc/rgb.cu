@@ -41,7 +41,7 @@ constexpr int kMaxThreads = 320;  // consumer threads per CTA (+ 2 producer warp
 constexpr int kMaxThreadsFF = 480;  // fused step: one CTA per SM with the force-field warps
 constexpr int kMaxStages = 6;
 constexpr size_t kSmemPerSm = 227 * 1024;  // opt-in dynamic shared memory per CTA on sm_100
-constexpr int kDefaultRpt = 8;
+constexpr int kDefaultRpt = 8;  // rows per thread per band (rolling 3-row register window)
 constexpr int kFFWarps = 4;     // force-field warps per CTA in the fused sensor step
 
 __host__ __device__ constexpr int term_index(int i, int j) { return (i + j) * (i + j + 1) / 2 + j; }

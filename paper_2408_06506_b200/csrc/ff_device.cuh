@@ -44,6 +44,7 @@ __device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y
 
 struct Grid {
   const double4* __restrict__ cells;  // {d, gx, gy, gz} per cell, z fastest
+  const double* __restrict__ values;  // d only, compact (8 B per cell): the mask path's gathers
   int nx, ny, nz;
   double ox, oy, oz, spacing, inv_spacing;
 };
@@ -107,7 +108,7 @@ __device__ __forceinline__ size_t corner(const Grid& g, const Cell& c, int k) {
 __device__ __forceinline__ double interp_d(const Grid& g, const Cell& c) {
   double v[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) v[k] = __ldg(&g.cells[corner(g, c, k)].x);
+  for (int k = 0; k < 8; ++k) v[k] = __ldg(g.values + corner(g, c, k));
   const double d00 = add_rn(mul_rn(v[0], c.ux), mul_rn(v[4], c.wx));
   const double d10 = add_rn(mul_rn(v[2], c.ux), mul_rn(v[6], c.wx));
   const double d01 = add_rn(mul_rn(v[1], c.ux), mul_rn(v[5], c.wx));
@@ -437,7 +438,7 @@ __device__ __forceinline__ void frame_setup_warp(const FFArgs<OutT>& A, int64_t 
 __device__ __forceinline__ double interp_d_fast(const Grid& g, const Cell& c) {
   double v[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) v[k] = __ldg(&g.cells[corner(g, c, k)].x);
+  for (int k = 0; k < 8; ++k) v[k] = __ldg(g.values + corner(g, c, k));
   const double d00 = fma(c.wx, v[4] - v[0], v[0]);
   const double d10 = fma(c.wx, v[6] - v[2], v[2]);
   const double d01 = fma(c.wx, v[5] - v[1], v[1]);
@@ -464,6 +465,7 @@ __device__ __forceinline__ V3 exact_rel(const Grid& g, const double* __restrict_
 inline Grid make_grid(tacsl_sdf_t sdf) {
   Grid g;
   g.cells = sdf->grid;
+  g.values = sdf->values;
   g.nx = sdf->dims[0];
   g.ny = sdf->dims[1];
   g.nz = sdf->dims[2];

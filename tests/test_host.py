@@ -99,3 +99,24 @@ def test_reference_depth_bit_identical_to_env_background():
     cam = camera_for_sensor(spec)
     assert np.array_equal(cam.rays(), z["cam_dirs"])
     assert np.array_equal(reference_depth(cam, spec), z["background"])
+
+
+def test_host_quaternion_helpers_match_the_oracle_bit_for_bit():
+    """transforms.py (used for the env's relative peg poses) against the
+    oracle's restatement of transforms.py:17-47, on random inputs."""
+    from oracle import gelsim_oracle as O
+    from paper_2408_06506_b200 import transforms as T
+    rng = np.random.default_rng(11)
+    q = rng.normal(size=(257, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    v = rng.normal(size=(257, 3))
+    assert np.array_equal(T.quat_rotate(q, v), O.quat_rotate(q, v))
+    assert np.array_equal(T.quat_rotate_inv(q, v), O.quat_rotate_inv(q, v))
+    r = rng.normal(size=(257, 4))
+    a, b = q, r
+    aw, ax, ay, az = a.T
+    bw, bx, by, bz = b.T
+    ref = np.stack([aw * bw - ax * bx - ay * by - az * bz, aw * bx + ax * bw + ay * bz - az * by,
+                    aw * by - ax * bz + ay * bw + az * bx, aw * bz + ax * by - ay * bx + az * bw], axis=-1)
+    assert np.array_equal(T.quat_mul(a, b), ref)
+    assert np.array_equal(T.quat_conj(q), q * np.array([1.0, -1.0, -1.0, -1.0]))

@@ -13,7 +13,7 @@ plus ``SensorArray`` (one batched RGB + force-field step for E envs x S
 sensors) and ``patch()`` to rebind the reference's names.  There is no CPU
 fallback: without a B200 every compute call raises RuntimeError.
 """
-from . import formats
+from . import envs, formats
 from .augment import AugmentConfig, augment
 from .binned import BinnedPolyLut, depth_to_rgb_binned
 from .depth import render_depth
@@ -39,7 +39,7 @@ __all__ = [
     "DimensionMismatch", "GelsimError", "InvalidQuery", "LutResolutionMismatch",
     "SdfGrid", "SdfQuery", "query_sdf", "read_sdf_cache", "write_sdf_cache",
     "patch", "unpatch", "SensorArray", "shard_range",
-    "formats", "AugmentConfig", "augment", "BinnedPolyLut", "depth_to_rgb_binned", "render_depth", "DepthImage", "PolyLut", "depth_to_rgb", "monomial_exponents", "synthetic_lut", "to_uint8",
+    "envs", "formats", "AugmentConfig", "augment", "BinnedPolyLut", "depth_to_rgb_binned", "render_depth", "DepthImage", "PolyLut", "depth_to_rgb", "monomial_exponents", "synthetic_lut", "to_uint8",
     "TactileCamera", "TactileSensorSpec", "camera_for_sensor", "reference_depth",
     "ForceField", "PenaltyParams", "TactilePointGrid", "compute_force_field", "net_wrench",
     "penalty_forces", "sample_tactile_points",

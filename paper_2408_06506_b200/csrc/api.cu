@@ -129,6 +129,8 @@ int tacsl_sdf_create(int device, const double* values, const double* gradients, 
   if (!tacsl_device_supported(device))
     return set_error(TACSL_ERR_NO_DEVICE, "sdf_create: device is not an sm_100 (B200) GPU");
   const size_t n = (size_t)dims[0] * dims[1] * dims[2];
+  if (n >= ((size_t)1 << 31))  // kernels index cells with 32-bit ints
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "sdf_create: grids are limited to 2^31 cells");
   std::vector<double4> host(n);
   for (size_t i = 0; i < n; ++i)
     host[i] = make_double4(values[i], gradients[3 * i + 0], gradients[3 * i + 1], gradients[3 * i + 2]);

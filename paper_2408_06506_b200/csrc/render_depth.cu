@@ -35,10 +35,10 @@ struct RenderParams {
 
 // correctly rounded a / spacing (Markstein: y = RN(1/b), q = RN(a y), one
 // exact-remainder correction), as in force_field.cu
-__device__ __forceinline__ double div_spacing(double a, const RenderParams& P) {
-  const double q = mul_rn(a, P.inv_spacing);
-  const double r = __fma_rn(-q, P.spacing, a);
-  return __fma_rn(r, P.inv_spacing, q);
+__device__ __forceinline__ double div_spacing(double a, double spacing, double inv_spacing) {
+  const double q = mul_rn(a, inv_spacing);
+  const double r = __fma_rn(-q, spacing, a);
+  return __fma_rn(r, inv_spacing, q);
 }
 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }  // np.maximum w/o NaNs
@@ -48,6 +48,11 @@ __global__ void __launch_bounds__(256) render_depth_kernel(const RenderParams P,
                                                            const double* __restrict__ background,
                                                            const double* __restrict__ envp, int64_t n_envs,
                                                            double* __restrict__ out64, float* __restrict__ out32) {
+  // the march's constants as locals (registers, not per-step constant-bank loads)
+  const double gox = P.gox, goy = P.goy, goz = P.goz, hix = P.hix, hiy = P.hiy, hiz = P.hiz;
+  const double cx = P.cx, cy = P.cy, cz = P.cz, spacing = P.spacing, inv_spacing = P.inv_spacing, tol = P.tol;
+  const int nxm = P.nx - 2, nym = P.ny - 2, nzm = P.nz - 2, ny = P.ny, nz = P.nz, max_steps = P.max_steps;
+  const double* __restrict__ values = P.values;
   // grid: y over envs, x over an env's rays (no 64-bit division per ray)
   for (int64_t e = blockIdx.y; e < n_envs; e += gridDim.y)
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n_rays; r += gridDim.x * blockDim.x) {
@@ -80,30 +85,30 @@ __global__ void __launch_bounds__(256) render_depth_kernel(const RenderParams P,
       const double r10 = __ldg(ep + 6), r11 = __ldg(ep + 7), r12 = __ldg(ep + 8);
       const double r20 = __ldg(ep + 9), r21 = __ldg(ep + 10), r22 = __ldg(ep + 11);
       double t = t_start;
-      for (int step = 0; step < P.max_steps; ++step) {
-        const double wx = sub_rn(add_rn(P.cx, mul_rn(dx, t)), px);
-        const double wy = sub_rn(add_rn(P.cy, mul_rn(dy, t)), py);
-        const double wz = sub_rn(add_rn(P.cz, mul_rn(dz, t)), pz);
+      for (int step = 0; step < max_steps; ++step) {
+        const double wx = sub_rn(add_rn(cx, mul_rn(dx, t)), px);
+        const double wy = sub_rn(add_rn(cy, mul_rn(dy, t)), py);
+        const double wz = sub_rn(add_rn(cz, mul_rn(dz, t)), pz);
         // R^T w: sensor -> object frame
         const double ox = add_rn(add_rn(mul_rn(r00, wx), mul_rn(r10, wy)), mul_rn(r20, wz));
         const double oy = add_rn(add_rn(mul_rn(r01, wx), mul_rn(r11, wy)), mul_rn(r21, wz));
         const double oz = add_rn(add_rn(mul_rn(r02, wx), mul_rn(r12, wy)), mul_rn(r22, wz));
         double d;
-        if (ox < P.gox || oy < P.goy || oz < P.goz || ox > P.hix || oy > P.hiy || oz > P.hiz) {
+        if (ox < gox || oy < goy || oz < goz || ox > hix || oy > hiy || oz > hiz) {
           // outside the grid: distance to the box is a safe step (depth.py:205-210)
-          const double bx = add_rn(dmax(sub_rn(P.gox, ox), 0.0), dmax(sub_rn(ox, P.hix), 0.0));
-          const double by = add_rn(dmax(sub_rn(P.goy, oy), 0.0), dmax(sub_rn(oy, P.hiy), 0.0));
-          const double bz = add_rn(dmax(sub_rn(P.goz, oz), 0.0), dmax(sub_rn(oz, P.hiz), 0.0));
-          d = dmax(__dsqrt_rn(add_rn(add_rn(mul_rn(bx, bx), mul_rn(by, by)), mul_rn(bz, bz))), P.spacing);
+          const double bx = add_rn(dmax(sub_rn(gox, ox), 0.0), dmax(sub_rn(ox, hix), 0.0));
+          const double by = add_rn(dmax(sub_rn(goy, oy), 0.0), dmax(sub_rn(oy, hiy), 0.0));
+          const double bz = add_rn(dmax(sub_rn(goz, oz), 0.0), dmax(sub_rn(oz, hiz), 0.0));
+          d = dmax(__dsqrt_rn(add_rn(add_rn(mul_rn(bx, bx), mul_rn(by, by)), mul_rn(bz, bz))), spacing);
         } else {
-          const double gx = div_spacing(sub_rn(ox, P.gox), P);
-          const double gy = div_spacing(sub_rn(oy, P.goy), P);
-          const double gz = div_spacing(sub_rn(oz, P.goz), P);
-          const int ix = min((int)gx, P.nx - 2), iy = min((int)gy, P.ny - 2), iz = min((int)gz, P.nz - 2);
+          const double gx = div_spacing(sub_rn(ox, gox), spacing, inv_spacing);
+          const double gy = div_spacing(sub_rn(oy, goy), spacing, inv_spacing);
+          const double gz = div_spacing(sub_rn(oz, goz), spacing, inv_spacing);
+          const int ix = min((int)gx, nxm), iy = min((int)gy, nym), iz = min((int)gz, nzm);
           const double fx = sub_rn(gx, (double)ix), fy = sub_rn(gy, (double)iy), fz = sub_rn(gz, (double)iz);
           const double ux = sub_rn(1.0, fx), uy = sub_rn(1.0, fy), uz = sub_rn(1.0, fz);
-          const size_t sy = (size_t)P.nz, sx = (size_t)P.ny * P.nz;
-          const double* v = P.values + (size_t)ix * sx + (size_t)iy * sy + iz;
+          const int sy = nz, sx = ny * nz;  // grids stay below 2^31 cells (checked at upload)
+          const double* v = values + ((ix * ny + iy) * nz + iz);
           const double c00 = add_rn(mul_rn(__ldg(v), ux), mul_rn(__ldg(v + sx), fx));
           const double c10 = add_rn(mul_rn(__ldg(v + sy), ux), mul_rn(__ldg(v + sx + sy), fx));
           const double c01 = add_rn(mul_rn(__ldg(v + 1), ux), mul_rn(__ldg(v + sx + 1), fx));
@@ -112,7 +117,7 @@ __global__ void __launch_bounds__(256) render_depth_kernel(const RenderParams P,
           const double c1 = add_rn(mul_rn(c01, uy), mul_rn(c11, fy));
           d = add_rn(mul_rn(c0, uz), mul_rn(c1, fz));
         }
-        if (d < P.tol) {
+        if (d < tol) {
           if (t < depth) depth = t;
           break;
         }

@@ -58,7 +58,7 @@ __device__ __forceinline__ double4 ldg256(const double4* p) {
 
 // Cell location and trilinear weights of a query point (sdf.py:280-290)
 struct Cell {
-  size_t base;
+  int base;  // first corner's cell index (grids are capped at 2^31 cells at upload)
   double wx, wy, wz, ux, uy, uz;
   bool valid;
 };
@@ -89,7 +89,7 @@ __device__ __forceinline__ Cell locate_rel(const Grid& g, const double rx, const
   c.ux = sub_rn(1.0, c.wx);
   c.uy = sub_rn(1.0, c.wy);
   c.uz = sub_rn(1.0, c.wz);
-  c.base = ((size_t)ix * g.ny + iy) * g.nz + iz;
+  c.base = (ix * g.ny + iy) * g.nz + iz;
   return c;
 }
 
@@ -99,8 +99,8 @@ __device__ __forceinline__ Cell locate(const Grid& g, V3 p) {
 }
 
 // corner k = 4*dx + 2*dy + dz
-__device__ __forceinline__ size_t corner(const Grid& g, const Cell& c, int k) {
-  return c.base + (size_t)((k >> 2) & 1) * g.ny * g.nz + (size_t)((k >> 1) & 1) * g.nz + (k & 1);
+__device__ __forceinline__ int corner(const Grid& g, const Cell& c, int k) {
+  return c.base + ((k >> 2) & 1) * g.ny * g.nz + ((k >> 1) & 1) * g.nz + (k & 1);
 }
 
 // Trilinear distance, x then y then z lerps with every product and sum

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(MAXT, MINB) force_field_fast_kernel(const FFAr
       cell.ux = 1.0 - cell.wx;
       cell.uy = 1.0 - cell.wy;
       cell.uz = 1.0 - cell.wz;
-      cell.base = ((size_t)ix * g.ny + iy) * g.nz + iz;
+      cell.base = (ix * g.ny + iy) * g.nz + iz;
       d = interp_d_fast(g, cell);
       need_exact = fabs(d) < kDistMargin;
     }

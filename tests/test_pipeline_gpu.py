@@ -126,3 +126,32 @@ def test_host_pipeline_graph_matches_device_step():
     arr.replay_host()
     torch.cuda.synchronize()
     assert torch.equal(host["rgb"], ref[0].flip(0))
+
+
+@pytest.mark.parametrize("deg,size,S", [(4, (84, 61), 1), (3, (320, 240), 2)])
+def test_sensor_array_u8_and_f32_fp64_forces(deg, size, S):
+    """Both RGB outputs at once (u8 + float), float64 forces, LUT degrees 3-4,
+    an odd image height: every output against the oracle."""
+    E = 5
+    _, cam, bg, _, pts = synthetic.sensor_setup(size, (20, 25))
+    lut = synthetic.synthetic_lut(size, degree=deg, gradient_scale=synthetic.lut_scale(size))
+    sdf = synthetic.peg_grid((32, 32, 64))
+    depth = synthetic.depth_batch(cam, bg, E * S, config_id=33).reshape(E, S, size[1], size[0])
+    obj, sen = synthetic.peg_states(E, S, config_id=33)
+    arr = SensorArray(lut, sdf, pts, PenaltyParams(), E, S, ff_fp64=True, rgb_u8=True, rgb_f32=True)
+    arr.step(torch.from_numpy(depth).cuda(), torch.from_numpy(obj).cuda(),
+             torch.from_numpy(np.ascontiguousarray(sen)).cuda())
+    torch.cuda.synchronize()
+    r_rgb, r_fn, r_ft, r_force, r_torque = oracle_step(lut, pts, sdf, depth, obj, sen)
+    F = E * S
+    u8 = arr.rgb_u8.cpu().numpy().reshape(r_rgb.shape)
+    assert np.abs(u8.astype(int) - r_rgb.astype(int)).max() <= 1
+    f32 = arr.rgb_f32.cpu().numpy().reshape((F,) + r_rgb.shape[1:])
+    ref_f = O.depth_to_rgb(depth.reshape((F,) + depth.shape[2:]), lut.coeffs, lut.degree)
+    assert np.abs(f32 - ref_f).max() < 2e-5
+    assert arr.f_n.dtype == torch.float64
+    assert vec_close(arr.f_n.cpu().numpy().reshape(r_fn.shape), r_fn, 1e-9, atol=1e-12)[0]
+    assert vec_close(arr.f_t.cpu().numpy().reshape(r_ft.shape), r_ft, 1e-9, atol=1e-12)[0]
+    w = arr.wrench.cpu().numpy().reshape(F, 6)
+    np.testing.assert_allclose(w[:, :3], r_force, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(w[:, 3:], r_torque, rtol=1e-9, atol=1e-12)

@@ -62,6 +62,129 @@ __global__ void __launch_bounds__(128, MINB) force_field_kernel(const FFArgs<Out
   }
 }
 
+// ---- fast chain, per taxel (shared by the one-pass and two-pass kernels) ---
+struct FastCtx {
+  const Grid* g;
+  const double* a;  // FrameC::A in shared memory
+  const double* b;  // FrameC::b
+  double mx, my, mz;
+  const double* obj;
+  const double* sen;
+};
+
+// Distance of taxel p (and its cell): fast affine cell map + lerps, the
+// reference chain only when the fast values do not clear a decision.
+__device__ __forceinline__ double decide_taxel(const FastCtx& X, double px, double py, double pz, Cell& cell) {
+  const Grid& g = *X.g;
+  const double* a = X.a;
+  const double* b = X.b;
+  const double rx = fma(a[0], px, fma(a[1], py, fma(a[2], pz, b[0])));
+  const double ry = fma(a[3], px, fma(a[4], py, fma(a[5], pz, b[1])));
+  const double rz = fma(a[6], px, fma(a[7], py, fma(a[8], pz, b[2])));
+  const bool inside = (rx > kCellMargin) & (rx < X.mx - kCellMargin) & (ry > kCellMargin) &
+                      (ry < X.my - kCellMargin) & (rz > kCellMargin) & (rz < X.mz - kCellMargin);
+  const bool outside = (rx < -kCellMargin) | (rx > X.mx + kCellMargin) | (ry < -kCellMargin) |
+                       (ry > X.my + kCellMargin) | (rz < -kCellMargin) | (rz > X.mz + kCellMargin);
+  double d = __longlong_as_double(0x7ff0000000000000LL);  // +inf: outside the grid
+  bool need_exact = !(inside | outside);
+  if (inside) {
+    const int ix = (int)rx, iy = (int)ry, iz = (int)rz;  // floor: rel > 0 and < dims-1
+    cell.wx = rx - (double)ix;
+    cell.wy = ry - (double)iy;
+    cell.wz = rz - (double)iz;
+    cell.ux = 1.0 - cell.wx;
+    cell.uy = 1.0 - cell.wy;
+    cell.uz = 1.0 - cell.wz;
+    cell.base = (ix * g.ny + iy) * g.nz + iz;
+    d = interp_d_fast(g, cell);
+    need_exact = fabs(d) < kDistMargin;
+  }
+  if (need_exact) {  // rare: replay the reference chain for this taxel
+    const V3 r = exact_rel(g, X.obj, X.sen, v3(px, py, pz));
+    cell = locate_rel(g, r.x, r.y, r.z);
+    d = cell.valid ? interp_d(g, cell) : __longlong_as_double(0x7ff0000000000000LL);
+  }
+  return d;
+}
+
+// contact path on the per-frame matrices (field.py:109-119); forces in the
+// sensor frame
+template <typename OutT>
+__device__ __forceinline__ void contact_forces(const FFArgs<OutT>& A, const FrameC& C, const Grid& g,
+                                               const Cell& cell, double d, double px, double py, double pz, V3& fn,
+                                               V3& ft) {
+  const double* Ms = C.Ms;
+  const double* Mo = C.Mo;
+  const V3 rs = v3(fma(Ms[0], px, fma(Ms[1], py, Ms[2] * pz)), fma(Ms[3], px, fma(Ms[4], py, Ms[5] * pz)),
+                   fma(Ms[6], px, fma(Ms[7], py, Ms[8] * pz)));
+  const V3 pw = v3(rs.x + C.sp[0], rs.y + C.sp[1], rs.z + C.sp[2]);
+  const V3 ro = v3(pw.x - C.op[0], pw.y - C.op[1], pw.z - C.op[2]);
+  const V3 n = interp_n(g, cell);
+  const V3 nw = v3(fma(Mo[0], n.x, fma(Mo[1], n.y, Mo[2] * n.z)), fma(Mo[3], n.x, fma(Mo[4], n.y, Mo[5] * n.z)),
+                   fma(Mo[6], n.x, fma(Mo[7], n.y, Mo[8] * n.z)));
+  const V3 cs = cross(v3(C.sw[0], C.sw[1], C.sw[2]), rs);
+  const V3 co = cross(v3(C.ow[0], C.ow[1], C.ow[2]), ro);
+  const V3 xd = v3((C.sv[0] + cs.x) - (C.ov[0] + co.x), (C.sv[1] + cs.y) - (C.ov[1] + co.y),
+                   (C.sv[2] + cs.z) - (C.ov[2] + co.z));
+  const double d_dot = dot(nw, xd);
+  const V3 vt = v3(xd.x - d_dot * nw.x, xd.y - d_dot * nw.y, xd.z - d_dot * nw.z);
+  V3 fnw, ftw;
+  bool c2;
+  penalty(A.P, d, d_dot, nw, vt, fnw, ftw, c2);
+  // world -> sensor frame: Ms^T f
+  fn = v3(fma(Ms[0], fnw.x, fma(Ms[3], fnw.y, Ms[6] * fnw.z)), fma(Ms[1], fnw.x, fma(Ms[4], fnw.y, Ms[7] * fnw.z)),
+          fma(Ms[2], fnw.x, fma(Ms[5], fnw.y, Ms[8] * fnw.z)));
+  ft = v3(fma(Ms[0], ftw.x, fma(Ms[3], ftw.y, Ms[6] * ftw.z)), fma(Ms[1], ftw.x, fma(Ms[4], ftw.y, Ms[7] * ftw.z)),
+          fma(Ms[2], ftw.x, fma(Ms[5], ftw.y, Ms[8] * ftw.z)));
+}
+
+template <typename OutT>
+__device__ __forceinline__ void store_taxel(const FFArgs<OutT>& A, int64_t t, V3 fn, V3 ft, bool contact) {
+  const int64_t o = t * 3;
+  if (A.f_n) {
+    A.f_n[o + 0] = (OutT)fn.x;
+    A.f_n[o + 1] = (OutT)fn.y;
+    A.f_n[o + 2] = (OutT)fn.z;
+  }
+  if (A.f_t) {
+    A.f_t[o + 0] = (OutT)ft.x;
+    A.f_t[o + 1] = (OutT)ft.y;
+    A.f_t[o + 2] = (OutT)ft.z;
+  }
+  if (A.obs) {  // policy observation [f_n.z, f_t.x, f_t.y] (envs/peg_tasks.py:474-476)
+    A.obs[o + 0] = (float)fn.z;
+    A.obs[o + 1] = (float)ft.x;
+    A.obs[o + 2] = (float)ft.y;
+  }
+  if (A.contact) A.contact[t] = contact ? 1 : 0;
+}
+
+template <int MAXT>
+__device__ __forceinline__ void write_wrench(double* wrench, int64_t frame, double acc[6], double (*part)[6]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) acc[k] = warp_sum(acc[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) part[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double t = 0.0;
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int w = 0; w < nw; ++w) t += part[w][threadIdx.x];
+    wrench[frame * 6 + threadIdx.x] = t;
+  }
+}
+
+template <typename OutT>
+__device__ __forceinline__ FastCtx fast_ctx(const FFArgs<OutT>& A, const FrameC& C, int64_t frame) {
+  const Grid& g = A.grid;
+  const int64_t e = frame / A.n_sensors;
+  const int sidx = (int)(frame - e * A.n_sensors);
+  return FastCtx{&A.grid, C.A, C.b, (double)(g.nx - 1), (double)(g.ny - 1), (double)(g.nz - 1),
+                 A.obj_state + e * A.obj_stride, A.sen_state + e * A.sen_stride + (int64_t)sidx * 13};
+}
+
 // The same frame with the fast mask chain (ff_device.cuh, FrameC): per frame
 // the two poses fold into rel = A p + b and three rotation matrices in
 // shared memory; per taxel 9 FMAs give the cell coordinates, trilinear
@@ -74,73 +197,18 @@ __global__ void __launch_bounds__(MAXT, MINB) force_field_fast_kernel(const FFAr
   __shared__ double part[MAXT / 32][6];
   if (threadIdx.x < 32) frame_setup_warp(A, frame, C, threadIdx.x);
   __syncthreads();
-  const Grid& g = A.grid;
-  const double* a = C.A;  // read from shared memory per taxel: keeps 24 registers free
-  const double* b = C.b;
-  const double mx = (double)(g.nx - 1), my = (double)(g.ny - 1), mz = (double)(g.nz - 1);
-  const int64_t e = frame / A.n_sensors;
-  const int sidx = (int)(frame - e * A.n_sensors);
-  const double* obj = A.obj_state + e * A.obj_stride;
-  const double* sen = A.sen_state + e * A.sen_stride + (int64_t)sidx * 13;
+  const FastCtx X = fast_ctx(A, C, frame);
   const int64_t out_base = frame * (int64_t)A.n_taxels;
   double acc[6] = {0, 0, 0, 0, 0, 0};
   for (int i = threadIdx.x; i < A.n_taxels; i += blockDim.x) {
     const double* tp = A.taxels + 3 * i;
     const double px = __ldg(tp), py = __ldg(tp + 1), pz = __ldg(tp + 2);
-    const double rx = fma(a[0], px, fma(a[1], py, fma(a[2], pz, b[0])));
-    const double ry = fma(a[3], px, fma(a[4], py, fma(a[5], pz, b[1])));
-    const double rz = fma(a[6], px, fma(a[7], py, fma(a[8], pz, b[2])));
-    const bool inside = (rx > kCellMargin) & (rx < mx - kCellMargin) & (ry > kCellMargin) &
-                        (ry < my - kCellMargin) & (rz > kCellMargin) & (rz < mz - kCellMargin);
-    const bool outside = (rx < -kCellMargin) | (rx > mx + kCellMargin) | (ry < -kCellMargin) |
-                         (ry > my + kCellMargin) | (rz < -kCellMargin) | (rz > mz + kCellMargin);
     Cell cell;
-    double d = __longlong_as_double(0x7ff0000000000000LL);  // +inf: outside the grid
-    bool need_exact = !(inside | outside);
-    if (inside) {
-      const int ix = (int)rx, iy = (int)ry, iz = (int)rz;  // floor: rel > 0 and < dims-1
-      cell.wx = rx - (double)ix;
-      cell.wy = ry - (double)iy;
-      cell.wz = rz - (double)iz;
-      cell.ux = 1.0 - cell.wx;
-      cell.uy = 1.0 - cell.wy;
-      cell.uz = 1.0 - cell.wz;
-      cell.base = (ix * g.ny + iy) * g.nz + iz;
-      d = interp_d_fast(g, cell);
-      need_exact = fabs(d) < kDistMargin;
-    }
-    if (need_exact) {  // rare: replay the reference chain for this taxel
-      const V3 r = exact_rel(g, obj, sen, v3(px, py, pz));
-      cell = locate_rel(g, r.x, r.y, r.z);
-      d = cell.valid ? interp_d(g, cell) : __longlong_as_double(0x7ff0000000000000LL);
-    }
+    const double d = decide_taxel(X, px, py, pz, cell);
     V3 fn = v3(0.0, 0.0, 0.0), ft = v3(0.0, 0.0, 0.0);
     const bool contact = d < 0.0;  // field.py:64 (d is +inf outside the grid)
     if (contact) {
-      // contact path on the per-frame matrices (field.py:109-119)
-      const double* Ms = C.Ms;
-      const double* Mo = C.Mo;
-      const V3 rs = v3(fma(Ms[0], px, fma(Ms[1], py, Ms[2] * pz)), fma(Ms[3], px, fma(Ms[4], py, Ms[5] * pz)),
-                       fma(Ms[6], px, fma(Ms[7], py, Ms[8] * pz)));
-      const V3 pw = v3(rs.x + C.sp[0], rs.y + C.sp[1], rs.z + C.sp[2]);
-      const V3 ro = v3(pw.x - C.op[0], pw.y - C.op[1], pw.z - C.op[2]);
-      const V3 n = interp_n(g, cell);
-      const V3 nw = v3(fma(Mo[0], n.x, fma(Mo[1], n.y, Mo[2] * n.z)), fma(Mo[3], n.x, fma(Mo[4], n.y, Mo[5] * n.z)),
-                       fma(Mo[6], n.x, fma(Mo[7], n.y, Mo[8] * n.z)));
-      const V3 cs = cross(v3(C.sw[0], C.sw[1], C.sw[2]), rs);
-      const V3 co = cross(v3(C.ow[0], C.ow[1], C.ow[2]), ro);
-      const V3 xd = v3((C.sv[0] + cs.x) - (C.ov[0] + co.x), (C.sv[1] + cs.y) - (C.ov[1] + co.y),
-                       (C.sv[2] + cs.z) - (C.ov[2] + co.z));
-      const double d_dot = dot(nw, xd);
-      const V3 vt = v3(xd.x - d_dot * nw.x, xd.y - d_dot * nw.y, xd.z - d_dot * nw.z);
-      V3 fnw, ftw;
-      bool c2;
-      penalty(A.P, d, d_dot, nw, vt, fnw, ftw, c2);
-      // world -> sensor frame: Ms^T f
-      fn = v3(fma(Ms[0], fnw.x, fma(Ms[3], fnw.y, Ms[6] * fnw.z)), fma(Ms[1], fnw.x, fma(Ms[4], fnw.y, Ms[7] * fnw.z)),
-              fma(Ms[2], fnw.x, fma(Ms[5], fnw.y, Ms[8] * fnw.z)));
-      ft = v3(fma(Ms[0], ftw.x, fma(Ms[3], ftw.y, Ms[6] * ftw.z)), fma(Ms[1], ftw.x, fma(Ms[4], ftw.y, Ms[7] * ftw.z)),
-              fma(Ms[2], ftw.x, fma(Ms[5], ftw.y, Ms[8] * ftw.z)));
+      contact_forces(A, C, A.grid, cell, d, px, py, pz, fn, ft);
       const V3 f = v3(fn.x + ft.x, fn.y + ft.y, fn.z + ft.z);
       const V3 tq = cross(v3(px, py, pz), f);
       acc[0] += f.x;
@@ -150,39 +218,9 @@ __global__ void __launch_bounds__(MAXT, MINB) force_field_fast_kernel(const FFAr
       acc[4] += tq.y;
       acc[5] += tq.z;
     }
-    const int64_t o = (out_base + i) * 3;
-    if (A.f_n) {
-      A.f_n[o + 0] = (OutT)fn.x;
-      A.f_n[o + 1] = (OutT)fn.y;
-      A.f_n[o + 2] = (OutT)fn.z;
-    }
-    if (A.f_t) {
-      A.f_t[o + 0] = (OutT)ft.x;
-      A.f_t[o + 1] = (OutT)ft.y;
-      A.f_t[o + 2] = (OutT)ft.z;
-    }
-    if (A.obs) {  // policy observation [f_n.z, f_t.x, f_t.y] (envs/peg_tasks.py:474-476)
-      A.obs[o + 0] = (float)fn.z;
-      A.obs[o + 1] = (float)ft.x;
-      A.obs[o + 2] = (float)ft.y;
-    }
-    if (A.contact) A.contact[out_base + i] = contact ? 1 : 0;
+    store_taxel(A, out_base + i, fn, ft, contact);
   }
-  if (A.wrench) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) acc[k] = warp_sum(acc[k]);
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) part[warp][k] = acc[k];
-    __syncthreads();
-    if (threadIdx.x < 6) {
-      double t = 0.0;
-      const int nw = (blockDim.x + 31) >> 5;
-      for (int w = 0; w < nw; ++w) t += part[w][threadIdx.x];
-      A.wrench[frame * 6 + threadIdx.x] = t;
-    }
-  }
+  if (A.wrench) write_wrench<MAXT>(A.wrench, frame, acc, part);
 }
 
 __global__ void __launch_bounds__(256) query_sdf_kernel(const Grid grid, const double* __restrict__ pts, int64_t n,

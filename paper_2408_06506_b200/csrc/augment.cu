@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(256) augment_apply_kernel(const float* __restr
                                                             const double* __restrict__ params, int rep, float n0,
                                                             float n1, float n2, float* __restrict__ out) {
   const int HW = H * W;
+  const float invW = 1.0f / (float)W;
   const float hc = (float)((H - 1) / 2.0), wc = (float)((W - 1) / 2.0);
   for (int64_t img = blockIdx.y; img < n; img += gridDim.y) {
     const double* P = params + img * 16;
@@ -278,7 +279,17 @@ __global__ void __launch_bounds__(256) augment_apply_kernel(const float* __restr
     const double db = P[P_DB], dc = P[P_DC], ds = P[P_DS], dh = P[P_DH];
     const bool step_jitter = db != 0.0 || dc != 1.0 || ds != 1.0 || dh != 0.0;
     for (int rem = blockIdx.x * blockDim.x + threadIdx.x; rem < HW; rem += gridDim.x * blockDim.x) {
-      const int y = rem / W, x = rem - y * W;
+      // rem / W without an integer division: float quotient (exact inputs
+      // below 2^24 pixels per image, error < 1), then one correction
+      int y = __float2int_rz(__int2float_rn(rem) * invW);
+      int x = rem - y * W;
+      if (x < 0) {
+        --y;
+        x += W;
+      } else if (x >= W) {
+        ++y;
+        x -= W;
+      }
       float v[3];
       if (resample) {
         // _resample_bilinear (augment.py:121-140)
@@ -357,6 +368,8 @@ extern "C" int tacsl_augment(const float* images, int64_t n, int height, int wid
   if (!images || !params || !out || (rep && !nominal))
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: null pointer");
   if (images == out) return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: in-place is not supported");
+  if ((int64_t)height * width >= (1 << 24))
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: images are limited to 2^24 pixels");
   const int64_t hw = (int64_t)height * width;
   const int64_t total = n * hw;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(current_device()) * 16);

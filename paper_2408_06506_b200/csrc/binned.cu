@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kBinnedThreads) rgb_binned_kernel(const float*
     const float* up = r > 0 ? row - W : row;
     const float* dn = r < H - 1 ? row + W : row;
     const bool edge_row = (r == 0) || (r == H - 1);
-    const int by = (int)(((int64_t)r * bins_y) / H);
+    const int by = r * bins_y / H;  // 32-bit: r * bins_y < 2^31
     const float* cbase = cs + (size_t)by * bins_x * 3 * T;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kBinnedThreads) rgb_binned_vec_kernel(const fl
       }
       const float2 hx01 = make_float2((c.y - left) * m0, c.z - c.x);
       const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
-      const int yb = (int)(((int64_t)r * bins_y) / H) * bins_x;
+      const int yb = (r * bins_y) / H * bins_x;  // 32-bit: r * bins_y < 2^31 (bins_y <= H)
       float2 v01[3], v23[3];
       if (one_bin) {
         const float2* cs = dup + (size_t)(yb + b0) * 3 * T;

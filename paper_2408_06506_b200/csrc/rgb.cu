@@ -407,11 +407,11 @@ template <int DEG>
 __global__ void __launch_bounds__(256) rgb_scalar_kernel(const float* __restrict__ depth, int64_t n_images, int H,
                                                          int W, uint8_t* __restrict__ out_u8,
                                                          float* __restrict__ out_f32, const LutParams L) {
-  const int64_t total = n_images * (int64_t)H * W;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += stride) {
-    const int64_t img = p / ((int64_t)H * W);
-    const int rem = (int)(p - img * H * W);
+  // grid: y over images, x over an image's pixels (32-bit index math)
+  const int HW = H * W;
+  for (int64_t img = blockIdx.y; img < n_images; img += gridDim.y)
+  for (int rem = blockIdx.x * blockDim.x + threadIdx.x; rem < HW; rem += gridDim.x * blockDim.x) {
+    const int64_t p = img * HW + rem;
     const int r = rem / W;
     const int x = rem - r * W;
     const float* f = depth + img * (int64_t)H * W;
@@ -561,7 +561,10 @@ int dispatch(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f3
   }
   const int64_t total = n * (int64_t)H * W;
   int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(current_device()) * 16);
-  rgb_scalar_kernel<DEG><<<(unsigned)blocks, 256, 0, stream>>>(depth, n, H, W, u8, f32, L);
+  const unsigned gy = (unsigned)std::min<int64_t>(n, 65535);
+  const unsigned gx = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>(((int64_t)H * W + 255) / 256, (blocks + gy - 1) / gy));
+  rgb_scalar_kernel<DEG><<<dim3(gx, gy), 256, 0, stream>>>(depth, n, H, W, u8, f32, L);
   return check_launch("rgb_scalar_kernel");
 }
 

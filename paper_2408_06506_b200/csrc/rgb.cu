@@ -522,23 +522,78 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
       cache.push_back({H, W, lay.stages, groups});
     }
   }
-  lay = with_groups(lay, groups, W);
-  const int threads = bulk_threads(W, groups, FF);
-  const size_t smem = lay.bytes(U8);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-  if (per_sm <= 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: band ring does not fit in shared memory");
-  per_sm = std::min(per_sm, env_int("TACSL_RGB_CTAS_PER_SM", per_sm));
-  const int bands = (H + lay.band - 1) / lay.band;
-  const int64_t units = n * bands;
-  int64_t grid = std::min<int64_t>(units, (int64_t)sm_count(current_device()) * per_sm);
   const int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
   FFArgs<float> F{};
   if (FF) F = *ff;
   BinArgs B{};
   if (BIN) B = *bin;
-  kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, lay.groups, lay.stages, u8, f32, L,
-                                                  bulk_store, F, B);
+  // launch with (groups, CTAs per SM); 0 ctas = as many as fit
+  auto go = [&](int g, int ctas) -> int {
+    const Layout l = with_groups(lay, g, W);
+    const int threads = bulk_threads(W, g, FF);
+    const size_t smem = l.bytes(U8);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm <= 0) return -1;
+    if (ctas > 0) per_sm = std::min(per_sm, ctas);
+    const int bands = (H + l.band - 1) / l.band;
+    const int64_t grid = std::min<int64_t>(n * bands, (int64_t)sm_count(current_device()) * per_sm);
+    kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, l.groups, l.stages, u8, f32, L, bulk_store,
+                                                    F, B);
+    return 0;
+  };
+  int ctas = env_int("TACSL_RGB_CTAS_PER_SM", 0);
+  if constexpr (F32 && !U8 && !FF && !BIN) {
+    // The float-output path's best launch shape varies with the image size
+    // in ways the occupancy model does not capture (measured: 0.82 vs 1.08
+    // ms at 8192 x 240x320 between neighbouring shapes), so the first
+    // un-captured call per (H, W, batch-size octave) times the candidates
+    // on its own data and keeps the fastest.
+    static std::vector<std::array<int, 5>> tuned;  // H, W, log2(n) -> groups, ctas
+    const int nb = 63 - __builtin_clzll((unsigned long long)std::max<int64_t>(n, 1));
+    bool have = false;
+    for (const auto& t : tuned)
+      if (t[0] == H && t[1] == W && t[2] == nb) {
+        groups = t[3];
+        ctas = t[4];
+        have = true;
+      }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cap);
+    if (!have && !std::getenv("TACSL_RGB_GROUPS") && !std::getenv("TACSL_RGB_CTAS_PER_SM") &&
+        cap == cudaStreamCaptureStatusNone) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      float best_ms = 1e30f;
+      int best_g = groups, best_c = 0;
+      const int gmax = std::max(1, std::min(kMaxCons / QW, (H + RPT - 1) / RPT));
+      for (int g = 1; g <= gmax && g <= 4; ++g) {
+        if (with_groups(lay, g, W).bytes(U8) > kSmemPerSm) break;
+        for (int c = 1; c <= 4; ++c) {
+          if (go(g, c) < 0) break;  // warm-up launch
+          cudaEventRecord(e0, stream);
+          go(g, c);
+          go(g, c);
+          cudaEventRecord(e1, stream);
+          cudaEventSynchronize(e1);
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best_ms) {
+            best_ms = ms;
+            best_g = g;
+            best_c = c;
+          }
+        }
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      groups = best_g;
+      ctas = best_c;
+      tuned.push_back({H, W, nb, groups, ctas});
+    }
+  }
+  if (go(groups, ctas) < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: band ring does not fit in shared memory");
   return check_launch("rgb_bulk_kernel");
 }
 

@@ -212,16 +212,27 @@ __device__ __forceinline__ float rem1(float x) {
 }
 
 // _apply_color (augment.py:143-153), float32
-__device__ __forceinline__ void apply_color(float v[3], double b, double c, double s, double h) {
-  if (c != 1.0) {
-    const float cf = (float)c;
+// one _apply_color call's parameters, converted to float32 and their
+// "is this stage active" tests taken once per image, not per pixel
+struct ColorOp {
+  float b, c, s, h;
+  bool do_c, do_b, do_hsv;
+};
+
+__device__ __forceinline__ ColorOp color_op(double b, double c, double s, double h) {
+  return ColorOp{(float)b, (float)c, (float)s, (float)h, c != 1.0, b != 0.0, s != 1.0 || h != 0.0};
+}
+
+__device__ __forceinline__ void apply_color(float v[3], const ColorOp& op) {
+  if (op.do_c) {
+    const float cf = op.c;
     for (int k = 0; k < 3; ++k) v[k] = fadd(fmul(fsub(v[k], 0.5f), cf), 0.5f);
   }
-  if (b != 0.0) {
-    const float bf = (float)b;
+  if (op.do_b) {
+    const float bf = op.b;
     for (int k = 0; k < 3; ++k) v[k] = fadd(v[k], bf);
   }
-  if (s != 1.0 || h != 0.0) {
+  if (op.do_hsv) {
     // rgb_to_hsv (augment.py:88-103) of the clipped colour
     const float r = clip01(v[0]), g = clip01(v[1]), bl = clip01(v[2]);
     const float mx = fmaxf(fmaxf(r, g), bl), mn = fminf(fminf(r, g), bl);
@@ -236,8 +247,8 @@ __device__ __forceinline__ void apply_color(float v[3], double b, double c, doub
     constexpr float kInv6 = 0.16666667163372039794921875f;  // RN(1/6)
     hue = span > 0.f ? rem1(div_y(hue, 6.f, kInv6)) : 0.f;
     // hue shift and saturation scale (augment.py:150-151)
-    hue = rem1(fadd(hue, (float)h));
-    sat = clip01(fmul(sat, (float)s));
+    hue = rem1(fadd(hue, op.h));
+    sat = clip01(fmul(sat, op.s));
     // hsv_to_rgb (augment.py:106-118)
     const float h6 = fmul(hue, 6.f);
     const float fi = floorf(h6);
@@ -275,9 +286,10 @@ __global__ void __launch_bounds__(256) augment_apply_kernel(const float* __restr
     const float zf = (float)zoom, izf = __frcp_rn(zf), sxf = (float)sx, syf = (float)sy;
     const int p0 = (int)P[P_P0], p1 = (int)P[P_P1], p2 = (int)P[P_P2];
     const bool permute = p0 != 0 || p1 != 1 || p2 != 2;
-    const double b = P[P_B], c = P[P_C], sat = P[P_S], hue = P[P_H];
+    const ColorOp episode_op = color_op(P[P_B], P[P_C], P[P_S], P[P_H]);
     const double db = P[P_DB], dc = P[P_DC], ds = P[P_DS], dh = P[P_DH];
     const bool step_jitter = db != 0.0 || dc != 1.0 || ds != 1.0 || dh != 0.0;
+    const ColorOp step_op = color_op(db, dc, ds, dh);
     for (int rem = blockIdx.x * blockDim.x + threadIdx.x; rem < HW; rem += gridDim.x * blockDim.x) {
       // rem / W without an integer division: float quotient (exact inputs
       // below 2^24 pixels per image, error < 1), then one correction
@@ -320,8 +332,8 @@ __global__ void __launch_bounds__(256) augment_apply_kernel(const float* __restr
         v[1] = w1;
         v[2] = w2;
       }
-      apply_color(v, b, c, sat, hue);
-      if (step_jitter) apply_color(v, db, dc, ds, dh);
+      apply_color(v, episode_op);
+      if (step_jitter) apply_color(v, step_op);
       for (int k = 0; k < 3; ++k) v[k] = clip01(v[k]);
       const int64_t idx = img * (int64_t)HW + rem;
       if (rep == 2) {

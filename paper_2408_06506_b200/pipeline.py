@@ -132,11 +132,32 @@ class SensorArray:
         d = depth[sl]
         if self._smooth is not None:
             d = smoothing.separable_filter_device(d, self._taps, 1, out=self._smooth[sl])
-        depth_to_rgb_device(d, self.lut, out_u8=None if self.rgb_u8 is None else self.rgb_u8[sl],
-                            out_f32=None if self.rgb_f32 is None else self.rgb_f32[sl])
-        for lvl in range(1, self.levels):
-            d = smoothing.pyr_down_device(d, out=self._lvl_depth[lvl][sl])
-            depth_to_rgb_device(d, self._lvl_luts[lvl], out_u8=self.rgb_levels[lvl][sl])
+        if self.levels == 1:
+            depth_to_rgb_device(d, self.lut, out_u8=None if self.rgb_u8 is None else self.rgb_u8[sl],
+                                out_f32=None if self.rgb_f32 is None else self.rgb_f32[sl])
+            return
+        # pyramid: level l's shading (current stream) overlaps the next
+        # level's decimation (side stream); both only read level l's depth
+        t = _device.torch()
+        main = t.cuda.current_stream(self.device)
+        if getattr(self, "_pyr_stream", None) is None:
+            self._pyr_stream = t.cuda.Stream(device=self.device)
+        side = self._pyr_stream
+        luts = self._lvl_luts
+        for lvl in range(self.levels):
+            nxt = None
+            if lvl + 1 < self.levels:
+                side.wait_stream(main)  # level lvl's depth is ready
+                with t.cuda.stream(side):
+                    nxt = smoothing.pyr_down_device(d, out=self._lvl_depth[lvl + 1][sl])
+            if lvl == 0:
+                depth_to_rgb_device(d, luts[0], out_u8=None if self.rgb_u8 is None else self.rgb_u8[sl],
+                                    out_f32=None if self.rgb_f32 is None else self.rgb_f32[sl])
+            else:
+                depth_to_rgb_device(d, luts[lvl], out_u8=self.rgb_levels[lvl][sl])
+            if nxt is not None:
+                main.wait_stream(side)
+                d = nxt
 
     def _launch_ff(self, obj_state, sen_state):
         force_field_device(self.sdf, self.taxels, self.rows, self.cols, obj_state, sen_state, self.params,

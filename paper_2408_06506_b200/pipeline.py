@@ -5,8 +5,9 @@ This is the multi-sensor caller of the two hot-path kernels -- the role of
 ``PegEnvBatch._tactile_images`` / ``_tactile_ff`` (envs/peg_tasks.py:434-477)
 without their per-sensor Python loops: K1 runs once over all E*S depth maps
 and K2 once over all E*S force fields.  The two launches go to two streams so
-K2's float64 ALU work overlaps K1's HBM streaming; ``capture()`` records the
-pair in a CUDA graph so a step costs one graph launch.
+K2 fills the SMs K1's tail leaves idle; ``capture()`` records the pair in a
+CUDA graph so a step costs one graph launch, and ``capture_host()`` records
+a whole pipelined host-to-host step the same way.
 """
 from __future__ import annotations
 
@@ -280,10 +281,12 @@ class SensorArray:
 
 
 class TactileObservations:
-    """Batched tactile observations of the 2-finger peg env: the outputs of
-    ``PegEnvBatch._tactile_images`` (envs/peg_tasks.py:434-459, without the
-    optional augmentation) and ``_tactile_ff`` (peg_tasks.py:461-477) for all
-    E envs x S sensors in two launches, with no per-sensor Python loop.
+    """Batched tactile observations of the 2-finger peg env from given depth
+    maps and states: the outputs of ``PegEnvBatch._tactile_images``
+    (envs/peg_tasks.py:434-459, with the optional per-(env, episode, step)
+    augmentation) and ``_tactile_ff`` (peg_tasks.py:461-477) for all E envs x
+    S sensors, with no per-sensor Python loop.  (``envs.tactile_images``
+    also renders the depth maps from the env's poses.)
 
     images: (E, S, H, W, 3) float32 ("color" / "diff") or (E, S, H, W, 6)
     ("concat"); ff: (E, S, R, C, 3) float32 = [f_n.z, f_t.x, f_t.y] in each

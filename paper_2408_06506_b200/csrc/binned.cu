@@ -364,10 +364,12 @@ extern "C" int tacsl_depth_to_rgb_binned(tacsl_binned_lut_t lut, const float* de
                   !std::getenv("TACSL_BINNED_SCALAR") && !std::getenv("TACSL_BINNED_SIMPLE");
   for (int b = 1; b < lut->bins_x && pairs_ok; ++b)
     pairs_ok = (((int64_t)b * width + lut->bins_x - 1) / lut->bins_x) % 2 == 0;
-  // measured: the band pipeline wins for narrow bins (10-px bins at 240x320:
-  // 3.1 vs 4.0 ms per 8192 frames), the per-quad kernel for wide ones
-  // (40-px bins: 1.54 vs 2.07 ms), whose quads rarely straddle an edge
-  if (pairs_ok && width < 24 * lut->bins_x)
+  // measured (8192 frames 240x320, tools/bench_binned.py): at degree 2 the
+  // band pipeline keeps each thread's coefficients in registers and wins for
+  // every bin width (10-px bins 1.48 vs 3.84 ms, 40-px bins 1.27 vs 1.40 ms);
+  // at higher degrees it reads them through L1 and wins only for narrow bins,
+  // the per-quad kernel's quads rarely straddling a wide bin's edge
+  if (pairs_ok && (lut->degree == 2 || width < 24 * lut->bins_x || std::getenv("TACSL_BINNED_BAND")))
     return launch_rgb_binned(lut->pairs, lut->bins_y, lut->bins_x, lut->degree, depth, n_images, height, width,
                              rgb_u8, rgb_f32, s);
   switch (lut->degree) {

@@ -89,7 +89,7 @@ __device__ __forceinline__ float2 poly2_sat(const float (&c)[15], float2 hx, flo
   return out;
 }
 
-// poly2_sat with per-thread coefficient PAIRS (c, c) read through L1 (the
+// poly2_sat with per-thread coefficient PAIRS (c, c), in registers or L1 (the
 // binned LUT: each pixel pair's bin has its own table, K6)
 template <int DEG>
 __device__ __forceinline__ float2 poly2_sat_p(const float2* __restrict__ c, float2 hx, float2 hy) {
@@ -97,9 +97,9 @@ __device__ __forceinline__ float2 poly2_sat_p(const float2* __restrict__ c, floa
   float2 out = bc(0.f);
 #pragma unroll
   for (int i = DEG; i >= 0; --i) {
-    float2 p = __ldg(c + term_index(i, DEG - i));
+    float2 p = c[term_index(i, DEG - i)];
 #pragma unroll
-    for (int j = DEG - i - 1; j >= 0; --j) p = __ffma2_rn(p, hy, __ldg(c + term_index(i, j)));
+    for (int j = DEG - i - 1; j >= 0; --j) p = __ffma2_rn(p, hy, c[term_index(i, j)]);
     if (i == DEG) {
       acc = p;
     } else if (i > 0) {
@@ -291,9 +291,28 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
       float* of = F32 ? out_f32 + (((size_t)img * H + r0) * W + row_off) * och : nullptr;
       constexpr int T = (DEG + 1) * (DEG + 2) / 2;
       int yb = 0, ynext = 0;
+      // binned LUT: at degree 2 the thread's two coefficient sets (72 regs)
+      // live in registers and are reloaded only when its rows cross into the
+      // next y bin; higher degrees would spill and read them through L1
+      constexpr bool RC = BIN && DEG == 2;
+      float2 ca[RC ? 3 * T : 1], cb[RC ? 3 * T : 1];
+      const float2* pa = nullptr;
+      const float2* pb = nullptr;
+      auto load_bins = [&]() {
+        pa = B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T;
+        pb = B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T;
+        if constexpr (RC) {
+#pragma unroll
+          for (int i = 0; i < 3 * T; ++i) {
+            ca[i] = pa[i];
+            cb[i] = pb[i];
+          }
+        }
+      };
       if constexpr (BIN) {  // y bin of this thread's first row and the first row of the next bin
         yb = (r0 + lr0) * B.bins_y / H;
         ynext = ((yb + 1) * H + B.bins_y - 1) / B.bins_y;
+        load_bins();
       }
       // a missing neighbour row / column is read as the pixel itself (the
       // offsets select it), so there is no select or copy in the row loop
@@ -318,18 +337,21 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
         const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
         float2 r01, g01, b01, r23, g23, b23;
         if constexpr (BIN) {
-          while (r >= ynext) {  // rows cross into the next y bin (at most once per row)
-            ++yb;
-            ynext = ((yb + 1) * H + B.bins_y - 1) / B.bins_y;
+          if (r >= ynext) {  // rows cross into the next y bin
+            do {
+              ++yb;
+              ynext = ((yb + 1) * H + B.bins_y - 1) / B.bins_y;
+            } while (r >= ynext);
+            load_bins();
           }
-          const float2* pa = B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T;
-          const float2* pb = B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T;
-          r01 = poly2_sat_p<DEG>(pa, hx01, hy01);
-          g01 = poly2_sat_p<DEG>(pa + T, hx01, hy01);
-          b01 = poly2_sat_p<DEG>(pa + 2 * T, hx01, hy01);
-          r23 = poly2_sat_p<DEG>(pb, hx23, hy23);
-          g23 = poly2_sat_p<DEG>(pb + T, hx23, hy23);
-          b23 = poly2_sat_p<DEG>(pb + 2 * T, hx23, hy23);
+          const float2* qa = RC ? ca : pa;
+          const float2* qb = RC ? cb : pb;
+          r01 = poly2_sat_p<DEG>(qa, hx01, hy01);
+          g01 = poly2_sat_p<DEG>(qa + T, hx01, hy01);
+          b01 = poly2_sat_p<DEG>(qa + 2 * T, hx01, hy01);
+          r23 = poly2_sat_p<DEG>(qb, hx23, hy23);
+          g23 = poly2_sat_p<DEG>(qb + T, hx23, hy23);
+          b23 = poly2_sat_p<DEG>(qb + 2 * T, hx23, hy23);
         } else {
           r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
           g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);

@@ -1,4 +1,7 @@
-"""Time the binned-LUT kernel (K6) against K1 on config-3-sized batches."""
+"""Time the binned-LUT kernel (K6) against K1 on config-3-sized batches;
+each K6 shape is timed through its dispatch choice and both forced paths
+(TACSL_BINNED_BAND = band pipeline, TACSL_BINNED_SIMPLE = per-quad kernel)."""
+import os
 import sys
 from pathlib import Path
 
@@ -31,8 +34,16 @@ def timeit(fn, reps=10):
 
 b1 = device_binned_lut(vignetted_lut(lut, (6, 8)), d.device)
 b2 = device_binned_lut(vignetted_lut(lut, (24, 32)), d.device)
-for name, fn in (("K1 global LUT", lambda: depth_to_rgb_device(d, lut, out_u8=u8)),
-                 ("K6 binned 6x8", lambda: depth_to_rgb_binned_device(d, b1, out_u8=u8)),
-                 ("K6 binned 24x32", lambda: depth_to_rgb_binned_device(d, b2, out_u8=u8))):
+
+def run(name, fn):
     ms = timeit(fn)
     print(f"{name}: {ms:.3f} ms for {N} frames 240x320, {nbytes / ms / 1e6:.0f} GB/s")
+
+
+run("K1 global LUT", lambda: depth_to_rgb_device(d, lut, out_u8=u8))
+for tag, b in (("6x8", b1), ("24x32", b2)):
+    for mode in ("", "TACSL_BINNED_BAND", "TACSL_BINNED_SIMPLE"):
+        if mode:
+            os.environ[mode] = "1"
+        run(f"K6 binned {tag} {mode or 'dispatch'}", lambda: depth_to_rgb_binned_device(d, b, out_u8=u8))
+        os.environ.pop(mode, None)

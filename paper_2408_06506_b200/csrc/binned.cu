@@ -366,7 +366,7 @@ extern "C" int tacsl_depth_to_rgb_binned(tacsl_binned_lut_t lut, const float* de
     pairs_ok = (((int64_t)b * width + lut->bins_x - 1) / lut->bins_x) % 2 == 0;
   // measured (8192 frames 240x320, tools/bench_binned.py): at degree 2 the
   // band pipeline keeps each thread's coefficients in registers and wins for
-  // every bin width (10-px bins 1.48 vs 3.84 ms, 40-px bins 1.27 vs 1.40 ms);
+  // every bin width (10-px bins 1.40 vs 3.83 ms, 40-px bins 1.12 vs 1.40 ms);
   // at higher degrees it reads them through L1 and wins only for narrow bins,
   // the per-quad kernel's quads rarely straddling a wide bin's edge
   if (pairs_ok && (lut->degree == 2 || width < 24 * lut->bins_x || std::getenv("TACSL_BINNED_BAND")))

@@ -91,15 +91,16 @@ __device__ __forceinline__ float2 poly2_sat(const float (&c)[15], float2 hx, flo
 
 // poly2_sat with per-thread coefficient PAIRS (c, c), in registers or L1 (the
 // binned LUT: each pixel pair's bin has its own table, K6)
-template <int DEG>
+template <int DEG, bool LDG>
 __device__ __forceinline__ float2 poly2_sat_p(const float2* __restrict__ c, float2 hx, float2 hy) {
+  auto coef = [&](int t) { return LDG ? __ldg(c + t) : c[t]; };
   float2 acc = bc(0.f);
   float2 out = bc(0.f);
 #pragma unroll
   for (int i = DEG; i >= 0; --i) {
-    float2 p = c[term_index(i, DEG - i)];
+    float2 p = coef(term_index(i, DEG - i));
 #pragma unroll
-    for (int j = DEG - i - 1; j >= 0; --j) p = __ffma2_rn(p, hy, c[term_index(i, j)]);
+    for (int j = DEG - i - 1; j >= 0; --j) p = __ffma2_rn(p, hy, coef(term_index(i, j)));
     if (i == DEG) {
       acc = p;
     } else if (i > 0) {
@@ -274,6 +275,29 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
   int bidx = (int)(blockIdx.x - img * bands);
   int s = 0, k = 0;
   uint32_t full_phase = 0;
+  // binned LUT: at degree 2 the thread's two coefficient sets (72 regs) live
+  // in registers, tagged with their y bin, and are reloaded only when its rows
+  // enter another y bin -- the launch keeps each CTA on one band (grid a
+  // multiple of the band count), so that is rare; higher degrees would spill
+  // and read the coefficients through L1
+  constexpr int T = (DEG + 1) * (DEG + 2) / 2;
+  constexpr bool RC = BIN && DEG == 2;
+  float2 ca[RC ? 3 * T : 1], cb[RC ? 3 * T : 1];
+  int yb = 0, ynext = 0, loaded_yb = -1;
+  auto load_bins = [&]() {
+    if constexpr (RC) {
+      if (yb != loaded_yb) {
+        const float2* pa = B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T;
+        const float2* pb = B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T;
+#pragma unroll
+        for (int i = 0; i < 3 * T; ++i) {
+          ca[i] = pa[i];
+          cb[i] = pb[i];
+        }
+        loaded_yb = yb;
+      }
+    }
+  };
   for (; img < n_images; ++k) {
     const int r0 = bidx * band;
     const int nrows = min(band, H - r0);
@@ -289,26 +313,6 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
       uint32_t* op = reinterpret_cast<uint32_t*>(out_buf + (size_t)b * out_stage + row_off * 3);
       const int och = L.rep == 2 ? 6 : 3;  // float channels per output pixel
       float* of = F32 ? out_f32 + (((size_t)img * H + r0) * W + row_off) * och : nullptr;
-      constexpr int T = (DEG + 1) * (DEG + 2) / 2;
-      int yb = 0, ynext = 0;
-      // binned LUT: at degree 2 the thread's two coefficient sets (72 regs)
-      // live in registers and are reloaded only when its rows cross into the
-      // next y bin; higher degrees would spill and read them through L1
-      constexpr bool RC = BIN && DEG == 2;
-      float2 ca[RC ? 3 * T : 1], cb[RC ? 3 * T : 1];
-      const float2* pa = nullptr;
-      const float2* pb = nullptr;
-      auto load_bins = [&]() {
-        pa = B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T;
-        pb = B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T;
-        if constexpr (RC) {
-#pragma unroll
-          for (int i = 0; i < 3 * T; ++i) {
-            ca[i] = pa[i];
-            cb[i] = pb[i];
-          }
-        }
-      };
       if constexpr (BIN) {  // y bin of this thread's first row and the first row of the next bin
         yb = (r0 + lr0) * B.bins_y / H;
         ynext = ((yb + 1) * H + B.bins_y - 1) / B.bins_y;
@@ -344,14 +348,14 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
             } while (r >= ynext);
             load_bins();
           }
-          const float2* qa = RC ? ca : pa;
-          const float2* qb = RC ? cb : pb;
-          r01 = poly2_sat_p<DEG>(qa, hx01, hy01);
-          g01 = poly2_sat_p<DEG>(qa + T, hx01, hy01);
-          b01 = poly2_sat_p<DEG>(qa + 2 * T, hx01, hy01);
-          r23 = poly2_sat_p<DEG>(qb, hx23, hy23);
-          g23 = poly2_sat_p<DEG>(qb + T, hx23, hy23);
-          b23 = poly2_sat_p<DEG>(qb + 2 * T, hx23, hy23);
+          const float2* qa = RC ? ca : B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T;
+          const float2* qb = RC ? cb : B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T;
+          r01 = poly2_sat_p<DEG, !RC>(qa, hx01, hy01);
+          g01 = poly2_sat_p<DEG, !RC>(qa + T, hx01, hy01);
+          b01 = poly2_sat_p<DEG, !RC>(qa + 2 * T, hx01, hy01);
+          r23 = poly2_sat_p<DEG, !RC>(qb, hx23, hy23);
+          g23 = poly2_sat_p<DEG, !RC>(qb + T, hx23, hy23);
+          b23 = poly2_sat_p<DEG, !RC>(qb + 2 * T, hx23, hy23);
         } else {
           r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
           g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
@@ -561,7 +565,8 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
     if (per_sm <= 0) return -1;
     if (ctas > 0) per_sm = std::min(per_sm, ctas);
     const int bands = (H + l.band - 1) / l.band;
-    const int64_t grid = std::min<int64_t>(n * bands, (int64_t)sm_count(current_device()) * per_sm);
+    int64_t grid = std::min<int64_t>(n * bands, (int64_t)sm_count(current_device()) * per_sm);
+    if (BIN && grid > bands) grid -= grid % bands;  // each CTA stays on one band: its y bins stay loaded
     kern<<<(unsigned)grid, threads, smem, stream>>>(depth, n, H, W, l.groups, l.stages, u8, f32, L, bulk_store,
                                                     F, B);
     return 0;

@@ -106,21 +106,29 @@ def test_gpu_binned_errors():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("bins", [(24, 32), (12, 40), (3, 80)])
-def test_gpu_band_pipeline_binned_equals_simple_kernel(monkeypatch, bins):
-    """Narrow bins run on K1's band pipeline (rgb_bulk_kernel<..., BIN>), wide
-    ones on the per-quad kernel: both evaluate the same FMA sequence per
-    pixel, so they agree bit for bit."""
+@pytest.mark.parametrize("deg,bins,n", [(3, (24, 32), 6), (3, (12, 40), 6), (3, (3, 80), 6), (2, (24, 32), 300),
+                                        (2, (6, 8), 300), (2, (7, 40), 300), (2, (240, 2), 40), (2, (13, 16), 1)])
+def test_gpu_band_pipeline_binned_equals_simple_kernel(monkeypatch, deg, bins, n):
+    """K1's band pipeline (rgb_bulk_kernel<..., BIN>, forced for every bin
+    width here) and the per-quad kernel evaluate the same FMA sequence per
+    pixel, so they agree bit for bit.  At degree 2 the band pipeline keeps
+    each thread's coefficient sets in registers across rows and work units:
+    hundreds of images make every CTA revisit its band, and bin heights that
+    do not divide the 8-row thread blocks (7, 13 bins over 240 rows) make the
+    sets change inside a thread's rows."""
     import torch
     from paper_2408_06506_b200.binned import depth_to_rgb_binned_device
     size = (320, 240)
     d, lut = _setup(size, n=6, cid=95)
-    lut = synthetic.synthetic_lut(size, degree=3, gradient_scale=synthetic.lut_scale(size))
+    d = np.ascontiguousarray(d[np.arange(n) % len(d)] + (np.arange(n) % 7)[:, None, None].astype(np.float32) * 1e-4)
+    lut = synthetic.synthetic_lut(size, degree=deg, gradient_scale=synthetic.lut_scale(size))
     v = vignetted_lut(lut, bins=bins, falloff=0.3)
     dd = torch.from_numpy(d).cuda()
     a = torch.empty(dd.shape + (3,), dtype=torch.uint8, device="cuda")
     fa = torch.empty(dd.shape + (3,), dtype=torch.float32, device="cuda")
+    monkeypatch.setenv("TACSL_BINNED_BAND", "1")
     depth_to_rgb_binned_device(dd, v, out_u8=a, out_f32=fa)
+    monkeypatch.delenv("TACSL_BINNED_BAND")
     monkeypatch.setenv("TACSL_BINNED_SIMPLE", "1")
     b = torch.empty_like(a)
     fb = torch.empty_like(fa)

@@ -23,6 +23,7 @@
  *                           per-sensor reduction when `wrench` is non-NULL)
  *   tacsl_net_wrench        tactile/field.py:132-141 net_wrench (standalone)
  *   tacsl_render_depth      render/depth.py:88-134 render_depth (SDF sphere tracer)
+ *   tacsl_env_render_params envs/peg_tasks.py:440-442 + render/depth.py:105-121 (per-env render inputs)
  *
  * The reference has no FFI of its own (pure numpy); the Python module
  * paper_2408_06506_b200 binds these with ctypes behind the reference's
@@ -204,6 +205,16 @@ TACSL_API int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const doub
                                  double far_plane, double hit_tolerance, int max_steps,
                                  const double* env_params, int64_t n_envs, double* depth_f64,
                                  float* depth_f32, void* stream);
+
+/* The env caller's per-step render inputs on the device (replaces the host
+ * pose math of envs/peg_tasks.py:440-442 and render/depth.py:105-112, 121):
+ *   poses       (n_envs, 7 * n_sensors + 7) float64 per env: each sensor's
+ *               world pos[3], quat(w,x,y,z)[4], then the object's
+ *   env_params  (n_envs * n_sensors, 18) output rows for tacsl_render_depth,
+ *               env-major: the object pose in each sensor's frame, R, AABB
+ * Same float64 operation order as the reference's numpy, bit for bit. */
+TACSL_API int tacsl_env_render_params(tacsl_sdf_t sdf, const double* poses, int64_t n_envs, int n_sensors,
+                                      double* env_params, void* stream);
 
 /* -------------------------------------------------------- force field --- */
 /* Elementwise penalty formulas on `count` points, all float64:

@@ -58,6 +58,7 @@ SIGNATURES = {
     "tacsl_depth_to_rgb_binned": (c_int, [c_void_p, P, c_int64, c_int, c_int, P, P, c_void_p]),
     "tacsl_render_depth": (c_int, [c_void_p, P, P, c_int, c_int, P, c_double, c_double, c_double, c_int, P,
                                    c_int64, P, P, c_void_p]),
+    "tacsl_env_render_params": (c_int, [c_void_p, P, c_int64, c_int, P, c_void_p]),
 }
 
 ABI_VERSION = 1

@@ -131,6 +131,108 @@ __global__ void __launch_bounds__(256) render_depth_kernel(const RenderParams P,
   }
 }
 
+// ------------------------------------------------ per-env render inputs ---
+// The env caller's host pose math on the device, operation for operation in
+// float64 (separately rounded, numpy's order), so K3 sees bit-identical
+// inputs:
+//   object pose in sensor s's frame   envs/peg_tasks.py:440-442
+//     pos  = quat_rotate(conj(q_s), p_obj - p_s)   transforms.py:30-47
+//     quat = quat_mul(conj(q_s), q_obj)            transforms.py:17-24
+//   env_params row (pos, R, AABB)      render/depth.py:105-112, 121
+//     R = quat_to_mat(quat)  (q / |q|, |q|^2 summed left to right)
+//     lo / hi = min / max over the 8 grid-box corners rotated into the frame
+struct Q4 {
+  double w, x, y, z;
+};
+struct D3 {
+  double x, y, z;
+};
+
+__device__ __forceinline__ D3 cross_rn(D3 a, D3 b) {  // np.cross / transforms._cross component order
+  return D3{sub_rn(mul_rn(a.y, b.z), mul_rn(a.z, b.y)), sub_rn(mul_rn(a.z, b.x), mul_rn(a.x, b.z)),
+            sub_rn(mul_rn(a.x, b.y), mul_rn(a.y, b.x))};
+}
+
+// v + w t + q_v x t with t = 2 q_v x v  (left to right)
+__device__ __forceinline__ D3 quat_rotate_rn(Q4 q, D3 v) {
+  const D3 qv{q.x, q.y, q.z};
+  D3 t = cross_rn(qv, v);
+  t = D3{mul_rn(2.0, t.x), mul_rn(2.0, t.y), mul_rn(2.0, t.z)};
+  const D3 c = cross_rn(qv, t);
+  return D3{add_rn(add_rn(v.x, mul_rn(q.w, t.x)), c.x), add_rn(add_rn(v.y, mul_rn(q.w, t.y)), c.y),
+            add_rn(add_rn(v.z, mul_rn(q.w, t.z)), c.z)};
+}
+
+__device__ __forceinline__ Q4 quat_mul_rn(Q4 a, Q4 b) {
+  return Q4{sub_rn(sub_rn(sub_rn(mul_rn(a.w, b.w), mul_rn(a.x, b.x)), mul_rn(a.y, b.y)), mul_rn(a.z, b.z)),
+            sub_rn(add_rn(add_rn(mul_rn(a.w, b.x), mul_rn(a.x, b.w)), mul_rn(a.y, b.z)), mul_rn(a.z, b.y)),
+            add_rn(add_rn(sub_rn(mul_rn(a.w, b.y), mul_rn(a.x, b.z)), mul_rn(a.y, b.w)), mul_rn(a.z, b.x)),
+            add_rn(sub_rn(add_rn(mul_rn(a.w, b.z), mul_rn(a.x, b.y)), mul_rn(a.y, b.x)), mul_rn(a.z, b.w))};
+}
+
+struct Box {
+  double lo[3], hi[3];  // grid-box corner coordinates: origin, origin + spacing * (dims - 1)
+};
+
+__global__ void __launch_bounds__(128) env_render_params_kernel(const double* __restrict__ poses, int64_t n_envs,
+                                                                int n_sensors, const Box box,
+                                                                double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (env, sensor)
+  if (i >= n_envs * n_sensors) return;
+  const int64_t e = i / n_sensors;
+  const int s = (int)(i - e * n_sensors);
+  const int stride = 7 * n_sensors + 7;
+  const double* row = poses + e * stride;
+  const double* sp = row + 7 * s;
+  const double* op = row + 7 * n_sensors;
+  // conj(q_s) = q_s * [1, -1, -1, -1]
+  const Q4 qc{mul_rn(sp[3], 1.0), mul_rn(sp[4], -1.0), mul_rn(sp[5], -1.0), mul_rn(sp[6], -1.0)};
+  const D3 d{sub_rn(op[0], sp[0]), sub_rn(op[1], sp[1]), sub_rn(op[2], sp[2])};
+  const D3 pos = quat_rotate_rn(qc, d);
+  const Q4 q = quat_mul_rn(qc, Q4{op[3], op[4], op[5], op[6]});
+  double* o = out + i * 18;
+  o[0] = pos.x;
+  o[1] = pos.y;
+  o[2] = pos.z;
+  // R = quat_to_mat(q)
+  const double n = __dsqrt_rn(add_rn(add_rn(add_rn(mul_rn(q.w, q.w), mul_rn(q.x, q.x)), mul_rn(q.y, q.y)),
+                                     mul_rn(q.z, q.z)));
+  const double w = __ddiv_rn(q.w, n), x = __ddiv_rn(q.x, n), y = __ddiv_rn(q.y, n), z = __ddiv_rn(q.z, n);
+  const double xx = mul_rn(x, x), yy = mul_rn(y, y), zz = mul_rn(z, z);
+  const double xy = mul_rn(x, y), xz = mul_rn(x, z), yz = mul_rn(y, z);
+  const double wx = mul_rn(w, x), wy = mul_rn(w, y), wz = mul_rn(w, z);
+  o[3] = sub_rn(1.0, mul_rn(2.0, add_rn(yy, zz)));
+  o[4] = mul_rn(2.0, sub_rn(xy, wz));
+  o[5] = mul_rn(2.0, add_rn(xz, wy));
+  o[6] = mul_rn(2.0, add_rn(xy, wz));
+  o[7] = sub_rn(1.0, mul_rn(2.0, add_rn(xx, zz)));
+  o[8] = mul_rn(2.0, sub_rn(yz, wx));
+  o[9] = mul_rn(2.0, sub_rn(xz, wy));
+  o[10] = mul_rn(2.0, add_rn(yz, wx));
+  o[11] = sub_rn(1.0, mul_rn(2.0, add_rn(xx, yy)));
+  // AABB of the rotated grid-box corners (unnormalised quaternion, as
+  // quat_rotate is called on it), corners in meshgrid 'ij' order
+  D3 lo{0, 0, 0}, hi{0, 0, 0};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const D3 v{(c & 4) ? box.hi[0] : box.lo[0], (c & 2) ? box.hi[1] : box.lo[1], (c & 1) ? box.hi[2] : box.lo[2]};
+    D3 r = quat_rotate_rn(q, v);
+    r = D3{add_rn(r.x, pos.x), add_rn(r.y, pos.y), add_rn(r.z, pos.z)};
+    if (c == 0) {
+      lo = hi = r;
+    } else {
+      lo = D3{dmin(r.x, lo.x), dmin(r.y, lo.y), dmin(r.z, lo.z)};
+      hi = D3{dmax(r.x, hi.x), dmax(r.y, hi.y), dmax(r.z, hi.z)};
+    }
+  }
+  o[12] = lo.x;
+  o[13] = lo.y;
+  o[14] = lo.z;
+  o[15] = hi.x;
+  o[16] = hi.y;
+  o[17] = hi.z;
+}
+
 }  // namespace
 }  // namespace tacsl
 
@@ -176,4 +278,21 @@ extern "C" int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const dou
   render_depth_kernel<<<dim3(gx, gy), 256, 0, (cudaStream_t)stream>>>(P, dirs, background, env_params, n_envs,
                                                                       depth_f64, depth_f32);
   return check_launch("render_depth_kernel");
+}
+
+extern "C" int tacsl_env_render_params(tacsl_sdf_t sdf, const double* poses, int64_t n_envs, int n_sensors,
+                                       double* env_params, void* stream) {
+  if (!sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "env_render_params: null SDF");
+  if (n_envs < 0 || n_sensors <= 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "env_render_params: bad sizes");
+  if (n_envs == 0) return TACSL_OK;
+  if (!poses || !env_params) return set_error(TACSL_ERR_INVALID_ARGUMENT, "env_render_params: null pointer");
+  Box box;
+  for (int k = 0; k < 3; ++k) {
+    box.lo[k] = sdf->origin[k] + sdf->spacing * 0.0;
+    box.hi[k] = sdf->origin[k] + sdf->spacing * (double)(sdf->dims[k] - 1);
+  }
+  const int64_t n = n_envs * n_sensors;
+  env_render_params_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(poses, n_envs, n_sensors,
+                                                                                          box, env_params);
+  return check_launch("env_render_params_kernel");
 }

@@ -71,6 +71,27 @@ class RayTable:
         self.background = _device.to_device(np.asarray(background, dtype=np.float64).reshape(-1), t.float64, device)
 
 
+def env_render_params_device(object_sdf, poses, n_sensors: int, out=None, stream=None):
+    """env_params on the device for E envs x n_sensors sensors from one
+    float64 CUDA tensor of world poses, (E, 7 * n_sensors + 7): each sensor's
+    pos[3] + quat[4], then the object's.  Row e * n_sensors + s is the object
+    pose in sensor s's frame (envs/peg_tasks.py:440-442) expanded into
+    env_params' layout -- bit-identical to env_params(object_sdf,
+    *relative poses) on the host."""
+    t = _device.torch()
+    E = int(poses.shape[0])
+    if poses.dtype != t.float64 or not poses.is_cuda or poses.shape[1] != 7 * n_sensors + 7:
+        raise ValueError("poses must be a float64 CUDA tensor of shape (E, 7 * n_sensors + 7)")
+    poses = poses.contiguous()
+    if out is None:
+        out = t.empty((E * n_sensors, 18), dtype=t.float64, device=poses.device)
+    dsdf = device_sdf(object_sdf, poses.device)
+    sh = _device.stream_handle(poses.device) if stream is None else stream
+    _lib.check(_lib.load().tacsl_env_render_params(dsdf.handle, poses.data_ptr(), E, int(n_sensors),
+                                                   out.data_ptr(), sh))
+    return out
+
+
 def render_depth_device(camera_table: RayTable, sdf, params, out_f64=None, out_f32=None, stream=None):
     """Device-level K3: params (E, 18) float64 CUDA tensor -> (E, H, W) depth."""
     dsdf = device_sdf(sdf, params.device)

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _device
 from .augment import augment_device
-from .depth import RayTable, env_params, render_depth_device
+from .depth import RayTable, env_render_params_device, render_depth_device
 from .render import tactile_image_obs_device
 from .tactile import device_taxels, force_field_device
 from .transforms import quat_conj, quat_mul, quat_rotate_inv
@@ -71,13 +71,25 @@ def _relative_peg_poses(env):
     return np.stack(pos, axis=1), np.stack(quat, axis=1)
 
 
+def _to_host(x) -> np.ndarray:
+    """Device tensor -> a fresh numpy array the caller owns, through a pinned
+    block of torch's host caching allocator: the copy runs at PCIe speed
+    (a pageable .cpu() staged the 0.47 GB image batch at ~2 GB/s), and the
+    block returns to the cache once the caller drops the array."""
+    t = _device.torch()
+    h = t.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    h.copy_(x, non_blocking=True)
+    t.cuda.current_stream(x.device).synchronize()
+    return h.numpy()
+
+
 def tactile_images(env) -> np.ndarray:
     """PegEnvBatch._tactile_images for all envs and both fingers:
     (E, 2, H, W, 3) float32 ("color" / "diff") or (E, 2, H, W, 6) ("concat"),
     as a fresh numpy array like the reference's (at 4096 envs that host copy
-    -- 0.47 GB -- dominates; GPU-resident consumers use
+    -- 0.47 GB over PCIe -- dominates; GPU-resident consumers use
     ``tactile_images_device``)."""
-    return tactile_images_device(env).cpu().numpy()
+    return _to_host(tactile_images_device(env))
 
 
 def tactile_images_device(env):
@@ -87,9 +99,16 @@ def tactile_images_device(env):
     c = env.cfg
     st = _state(env)
     E = st.E
-    rel_pos, rel_quat = _relative_peg_poses(env)
-    params = _device.to_device(env_params(env.peg_sdf, rel_pos.reshape(-1, 3), rel_quat.reshape(-1, 4)),
-                               t.float64, st.device)
+    # world poses up, the relative poses and render inputs on the device
+    # (the host-side restatement, _relative_peg_poses + env_params, is the
+    # parity reference: tests/test_env_golden_gpu.py)
+    b = env.bodies
+    cols = []
+    for s in range(N_SENSORS):
+        p, q = env._sensor_world_pose(s)
+        cols += [p, q]
+    poses = np.concatenate(cols + [b.pos[:, PEG], b.quat[:, PEG]], axis=1)
+    params = env_render_params_device(env.peg_sdf, _device.to_device(poses, t.float64, st.device), N_SENSORS)
     render_depth_device(st.rays, env.peg_sdf, params, out_f32=st.depth)
     rep = c.tactile_rep
     if c.augment is None:
@@ -107,7 +126,7 @@ def tactile_images_device(env):
 def tactile_ff(env) -> np.ndarray:
     """PegEnvBatch._tactile_ff: (E, 2, R, C, 3) float32 = [f_n.z, f_t.x, f_t.y]
     of each finger's force field in its sensor frame (fresh numpy array)."""
-    return tactile_ff_device(env).cpu().numpy()
+    return _to_host(tactile_ff_device(env))
 
 
 def tactile_ff_device(env):

@@ -151,3 +151,55 @@ def test_batched_env_methods_reproduce_the_env(env):
     assert vec_close(ff, env["ff"], 1e-5, atol=1e-7)[0]
     # second step reuses the cached device state
     assert np.array_equal(envs.tactile_images(e), images)
+
+
+def _world_poses(sen, obj):
+    """(E, 7 * S + 7) rows for env_render_params_device: sensor pos + quat,
+    then the object's."""
+    E, S = sen.shape[:2]
+    return np.concatenate([sen[:, :, 0:7].reshape(E, 7 * S), obj[:, 0:7]], axis=1)
+
+
+def test_env_render_params_on_device_bit_exact(env):
+    """The env's per-step host pose math on the device (K3's inputs): the
+    object pose in each finger's frame equals the reference env's recorded
+    relative pose bit for bit, R / AABB equal the host env_params of it, and
+    K3 fed straight from the device rows reproduces the env's depth maps."""
+    from paper_2408_06506_b200.depth import RayTable, env_params, env_render_params_device, render_depth_device
+    sdf = env["sdf"]
+    poses = torch.from_numpy(_world_poses(env["sen"], env["obj"])).cuda()
+    got = env_render_params_device(sdf, poses, 2).cpu().numpy()
+    assert np.array_equal(got[:, 0:3], env["rel_pos"].reshape(-1, 3))
+    host = env_params(sdf, env["rel_pos"].reshape(-1, 3), env["rel_quat"].reshape(-1, 4))
+    assert np.array_equal(got, host)
+    W, H = (int(v) for v in env["image_size"])
+    spec = TactileSensorSpec(image_size=(W, H))
+    cam = camera_for_sensor(spec)
+    rays = RayTable(cam, reference_depth(cam, spec), "cuda")
+    depth = torch.empty((got.shape[0], H, W), dtype=torch.float64, device="cuda")
+    render_depth_device(rays, sdf, torch.from_numpy(got).cuda(), out_f64=depth)
+    assert np.array_equal(depth.cpu().numpy().reshape(env["depth"].shape), env["depth"])
+
+
+@pytest.mark.parametrize("scale", [1e-3, 1.0, 30.0])
+def test_env_render_params_random_poses(env, scale):
+    """Random world poses (unnormalised quaternions, several magnitudes):
+    the device rows equal the host restatement (envs._relative_peg_poses +
+    depth.env_params, numpy's float64 order) bit for bit."""
+    from types import SimpleNamespace
+
+    from paper_2408_06506_b200.depth import env_params, env_render_params_device
+    from paper_2408_06506_b200.envs import PEG, _relative_peg_poses
+    rng = np.random.default_rng(int(scale * 1000) + 5)
+    E, S = 777, 2
+    sen = np.concatenate([rng.normal(size=(E, S, 3)) * scale, rng.normal(size=(E, S, 4)) * 0.7], axis=2)
+    obj = np.concatenate([rng.normal(size=(E, 3)) * scale, rng.normal(size=(E, 4)) * 1.3], axis=1)
+    pos = np.zeros((E, 4, 3))
+    quat = np.zeros((E, 4, 4))
+    pos[:, PEG], quat[:, PEG] = obj[:, 0:3], obj[:, 3:7]
+    fake = SimpleNamespace(bodies=SimpleNamespace(pos=pos, quat=quat),
+                           _sensor_world_pose=lambda s: (sen[:, s, 0:3], sen[:, s, 3:7]))
+    rp, rq = _relative_peg_poses(fake)
+    host = env_params(env["sdf"], rp.reshape(-1, 3), rq.reshape(-1, 4))
+    got = env_render_params_device(env["sdf"], torch.from_numpy(_world_poses(sen, obj)).cuda(), S).cpu().numpy()
+    assert np.array_equal(got, host)

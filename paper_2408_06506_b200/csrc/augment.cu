@@ -272,7 +272,9 @@ __device__ __forceinline__ void apply_color(float v[3], const ColorOp& op) {
 // Grid: x strides over an image's pixels, y over images, so the per-image
 // parameters and the branches they select are uniform across a CTA and no
 // 64-bit division is needed per pixel.
-__global__ void __launch_bounds__(256) augment_apply_kernel(const float* __restrict__ in, int64_t n, int H, int W,
+// 5 CTAs per SM caps it at 48 registers without spills (63 unbounded):
+// 1.74 vs 1.78 ms at 2048 x 240x320 (tools/bench_augment.py)
+__global__ void __launch_bounds__(256, 5) augment_apply_kernel(const float* __restrict__ in, int64_t n, int H, int W,
                                                             const double* __restrict__ params, int rep, float n0,
                                                             float n1, float n2, float* __restrict__ out) {
   const int HW = H * W;

@@ -203,3 +203,17 @@ def test_env_render_params_random_poses(env, scale):
     host = env_params(env["sdf"], rp.reshape(-1, 3), rq.reshape(-1, 4))
     got = env_render_params_device(env["sdf"], torch.from_numpy(_world_poses(sen, obj)).cuda(), S).cpu().numpy()
     assert np.array_equal(got, host)
+
+
+def test_env_render_params_shapes_and_errors(env):
+    """One sensor per env, an empty batch, and malformed pose tables."""
+    from paper_2408_06506_b200.depth import env_params, env_render_params_device
+    sen, obj = env["sen"][:, :1], env["obj"]
+    got = env_render_params_device(env["sdf"], torch.from_numpy(_world_poses(sen, obj)).cuda(), 1).cpu().numpy()
+    assert np.array_equal(got, env_params(env["sdf"], env["rel_pos"][:, 0], env["rel_quat"][:, 0]))
+    empty = env_render_params_device(env["sdf"], torch.zeros((0, 21), dtype=torch.float64, device="cuda"), 2)
+    assert empty.shape == (0, 18)
+    with pytest.raises(ValueError):
+        env_render_params_device(env["sdf"], torch.zeros((3, 20), dtype=torch.float64, device="cuda"), 2)
+    with pytest.raises(ValueError):
+        env_render_params_device(env["sdf"], torch.zeros((3, 21), dtype=torch.float32, device="cuda"), 2)

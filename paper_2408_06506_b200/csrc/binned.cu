@@ -299,8 +299,6 @@ extern "C" int tacsl_binned_lut_create(int device, const double* coeffs, int deg
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "binned_lut_create: bins must be in [1, image size]");
   const int T = (degree + 1) * (degree + 2) / 2;
   const int n_sets = bins_y * bins_x;
-  if (binned_smem(n_sets, T, width) > kBinnedMaxSmem)
-    return set_error(TACSL_ERR_INVALID_ARGUMENT, "binned_lut_create: too many bins for shared memory");
   if (!tacsl_device_supported(device))
     return set_error(TACSL_ERR_NO_DEVICE, "binned_lut_create: device is not an sm_100 (B200) GPU");
   std::vector<float> host((size_t)n_sets * 3 * T);
@@ -369,9 +367,19 @@ extern "C" int tacsl_depth_to_rgb_binned(tacsl_binned_lut_t lut, const float* de
   // every bin width (10-px bins 1.40 vs 3.83 ms, 40-px bins 1.12 vs 1.40 ms);
   // at higher degrees it reads them through L1 and wins only for narrow bins,
   // the per-quad kernel's quads rarely straddling a wide bin's edge
-  if (pairs_ok && (lut->degree == 2 || width < 24 * lut->bins_x || std::getenv("TACSL_BINNED_BAND")))
+  // the per-quad kernels stage the whole table in shared memory; the band
+  // pipeline reads it through registers / L1 and takes any table size
+  const int T = (lut->degree + 1) * (lut->degree + 2) / 2;
+  const bool table_fits = binned_smem(lut->bins_y * lut->bins_x, T, width) <= kBinnedMaxSmem;
+  if (pairs_ok &&
+      (lut->degree == 2 || width < 24 * lut->bins_x || !table_fits || std::getenv("TACSL_BINNED_BAND")))
     return launch_rgb_binned(lut->pairs, lut->bins_y, lut->bins_x, lut->degree, depth, n_images, height, width,
                              rgb_u8, rgb_f32, s);
+  if (!table_fits)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT,
+                     "depth_to_rgb_binned: this many bins need the band pipeline (width % 4 == 0, 16-B aligned "
+                     "buffers, every x-bin edge on an even column); the per-quad kernel's shared memory holds "
+                     "at most " + std::to_string(kBinnedMaxSmem / 1024) + " KB of table");
   switch (lut->degree) {
     case 2: return launch_binned<2>(lut, depth, n_images, rgb_u8, rgb_f32, s);
     case 3: return launch_binned<3>(lut, depth, n_images, rgb_u8, rgb_f32, s);

@@ -101,8 +101,27 @@ def test_gpu_binned_errors():
     with pytest.raises(LutResolutionMismatch):
         depth_to_rgb_binned(torch.from_numpy(d[..., :-1]).cuda().contiguous(), v)
     big = BinnedPolyLut(degree=4, coeffs=np.zeros((60, 80, 3, 15)), image_size=(80, 60))
-    with pytest.raises(ValueError):  # table larger than shared memory
+    with pytest.raises(ValueError):  # table larger than shared memory, odd x-bin edges: no kernel takes it
         depth_to_rgb_binned(torch.from_numpy(d).cuda(), big)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("deg,bins", [(4, (24, 32)), (3, (48, 40)), (4, (60, 40))])
+def test_gpu_large_tables_on_the_band_pipeline(deg, bins):
+    """Tables too large for the per-quad kernel's shared memory run on the
+    band pipeline, which reads the coefficients through L1 at degrees 3-4:
+    same results as the CPU restatement (uint8 within one step)."""
+    import torch
+    from paper_2408_06506_b200.binned import depth_to_rgb_binned
+    size = (320, 240)
+    d, _ = _setup(size, n=2, cid=97)
+    lut = synthetic.synthetic_lut(size, degree=deg, gradient_scale=synthetic.lut_scale(size))
+    v = vignetted_lut(lut, bins=bins, falloff=0.4)
+    ref = O.to_uint8(oracle_binned(d, v.coeffs, v.degree))
+    got = depth_to_rgb_binned(torch.from_numpy(d).cuda(), v, out_dtype=np.uint8).cpu().numpy()
+    diff = np.abs(got.astype(int) - ref.astype(int))
+    assert diff.max() <= 1 and (diff > 0).mean() < 1e-3
+    np.testing.assert_allclose(depth_to_rgb_binned(d, v), oracle_binned(d, v.coeffs, v.degree), rtol=0, atol=2e-6)
 
 
 @pytest.mark.gpu

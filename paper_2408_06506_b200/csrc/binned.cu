@@ -365,10 +365,11 @@ extern "C" int tacsl_depth_to_rgb_binned(tacsl_binned_lut_t lut, const float* de
   // measured (8192 frames 240x320, tools/bench_binned.py): at degree 2 the
   // band pipeline keeps each thread's coefficients in registers and wins for
   // every bin width (10-px bins 1.40 vs 3.83 ms, 40-px bins 1.12 vs 1.40 ms);
-  // at higher degrees it reads them through L1 and wins only for narrow bins,
-  // the per-quad kernel's quads rarely straddling a wide bin's edge
-  // the per-quad kernels stage the whole table in shared memory; the band
-  // pipeline reads it through registers / L1 and takes any table size
+  // at degrees 3-4 it reads them from its band's slice of the table in shared
+  // memory and wins for narrow bins only (degree 3, 10-px bins: 2.96 vs 6.84
+  // ms; 40-px bins: 2.23 vs 1.97 ms -- the per-quad kernel's quads rarely
+  // straddle a wide bin's edge).  The per-quad kernels stage the WHOLE table
+  // in shared memory, so larger tables go to the band pipeline regardless.
   const int T = (lut->degree + 1) * (lut->degree + 2) / 2;
   const bool table_fits = binned_smem(lut->bins_y * lut->bins_x, T, width) <= kBinnedMaxSmem;
   if (pairs_ok &&

@@ -134,7 +134,21 @@ __device__ __forceinline__ void shade(const LutParams& L, float hx, float hy, fl
 struct BinArgs {
   const float2* __restrict__ pairs;
   int bins_y, bins_x;
+  int tab_ybins;  // > 0: degrees 3-4 stage the band's y bins in shared memory (at most this many)
 };
+
+// y bins one band of `band` rows can touch (max over the bands of the image)
+inline int band_ybins(int H, int band, int bins_y) {
+  int m = 0;
+  for (int r0 = 0; r0 < H; r0 += band)
+    m = std::max(m, (std::min(r0 + band, H) - 1) * bins_y / H - r0 * bins_y / H + 1);
+  return m;
+}
+
+// barrier over the consumer warps only (the loader / storer warps never join)
+__device__ __forceinline__ void consumer_bar(int threads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+}
 
 struct Layout {
   int band, rpt, groups, stages;
@@ -298,11 +312,27 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
       }
     }
   };
+  // degrees 3-4: the y bins of the CTA's band staged in shared memory behind
+  // the ring (reloaded when the band changes -- rarely, see the launch)
+  float2* tab = reinterpret_cast<float2*>(out_buf + (U8 ? 2 * out_stage : 0));
+  int tab_band = -1, tab_y0 = 0;
   for (; img < n_images; ++k) {
     const int r0 = bidx * band;
     const int nrows = min(band, H - r0);
     const int b = k & 1;
     const bool active = lr0 < nrows;
+    if constexpr (BIN && !RC) {
+      if (B.tab_ybins > 0 && bidx != tab_band) {
+        const int y0 = r0 * B.bins_y / H;
+        const int cnt = ((nrows + r0 - 1) * B.bins_y / H - y0 + 1) * B.bins_x * 3 * T;
+        const float2* src = B.pairs + (size_t)y0 * B.bins_x * 3 * T;
+        consumer_bar(cons_warps * 32);  // every consumer is done with the previous band's table
+        for (int i = threadIdx.x; i < cnt; i += cons_warps * 32) tab[i] = src[i];
+        consumer_bar(cons_warps * 32);
+        tab_band = bidx;
+        tab_y0 = y0;
+      }
+    }
     mbar_wait_parity(&full[s], full_phase);
     if (U8 && k >= 2) mbar_wait_parity(&ofree[b], (uint32_t)((k >> 1) - 1) & 1u);
     if (active) {
@@ -348,14 +378,24 @@ __global__ void __launch_bounds__(FF ? kMaxThreadsFF + 64 + kFFWarps * 32 : kMax
             } while (r >= ynext);
             load_bins();
           }
-          const float2* qa = RC ? ca : B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T;
-          const float2* qb = RC ? cb : B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T;
-          r01 = poly2_sat_p<DEG, !RC>(qa, hx01, hy01);
-          g01 = poly2_sat_p<DEG, !RC>(qa + T, hx01, hy01);
-          b01 = poly2_sat_p<DEG, !RC>(qa + 2 * T, hx01, hy01);
-          r23 = poly2_sat_p<DEG, !RC>(qb, hx23, hy23);
-          g23 = poly2_sat_p<DEG, !RC>(qb + T, hx23, hy23);
-          b23 = poly2_sat_p<DEG, !RC>(qb + 2 * T, hx23, hy23);
+          auto eval = [&](auto ldg, const float2* qa, const float2* qb) {
+            constexpr bool G = decltype(ldg)::value;
+            r01 = poly2_sat_p<DEG, G>(qa, hx01, hy01);
+            g01 = poly2_sat_p<DEG, G>(qa + T, hx01, hy01);
+            b01 = poly2_sat_p<DEG, G>(qa + 2 * T, hx01, hy01);
+            r23 = poly2_sat_p<DEG, G>(qb, hx23, hy23);
+            g23 = poly2_sat_p<DEG, G>(qb + T, hx23, hy23);
+            b23 = poly2_sat_p<DEG, G>(qb + 2 * T, hx23, hy23);
+          };
+          if constexpr (RC) {
+            eval(std::false_type{}, ca, cb);
+          } else if (B.tab_ybins > 0) {
+            const int row = (yb - tab_y0) * B.bins_x;
+            eval(std::false_type{}, tab + (row + xba) * 3 * T, tab + (row + xbb) * 3 * T);
+          } else {
+            eval(std::true_type{}, B.pairs + (size_t)(yb * B.bins_x + xba) * 3 * T,
+                 B.pairs + (size_t)(yb * B.bins_x + xbb) * 3 * T);
+          }
         } else {
           r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
           g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
@@ -520,14 +560,24 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
   constexpr int kMaxCons = FF ? kMaxThreadsFF : kMaxThreads;
   if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), (int)kSmemPerSm)) return rc;
   std::lock_guard<std::mutex> lock(mu);
+  // binned LUT at degrees 3-4: the band's y bins in shared memory behind the
+  // ring when they fit (else the kernel reads the table through L1)
+  constexpr int T = (DEG + 1) * (DEG + 2) / 2;
+  bool use_tab = BIN && DEG > 2 && !std::getenv("TACSL_BINNED_L1");
+  auto tab_bytes = [&](int band) -> size_t {
+    return use_tab ? (size_t)band_ybins(H, band, bin->bins_y) * bin->bins_x * 3 * T * sizeof(float2) : 0;
+  };
+  auto need = [&](const Layout& l) { return l.bytes(U8) + tab_bytes(l.band); };
+  if (use_tab && need(with_groups(lay, 1, W)) > kSmemPerSm) use_tab = false;
   int groups = 0;
   if (const char* g = std::getenv("TACSL_RGB_GROUPS")) {
     groups = std::max(1, std::min(std::atoi(g), kMaxCons / QW));
-    while (groups > 1 && with_groups(lay, groups, W).bytes(U8) > kSmemPerSm) --groups;
-    while (lay.stages > 1 && with_groups(lay, groups, W).bytes(U8) > kSmemPerSm) --lay.stages;
+    while (groups > 1 && need(with_groups(lay, groups, W)) > kSmemPerSm) --groups;
+    while (lay.stages > 1 && need(with_groups(lay, groups, W)) > kSmemPerSm) --lay.stages;
   } else {
-    for (const auto& c : cache)
-      if (c[0] == H && c[1] == W && c[2] == lay.stages) groups = c[3];
+    if (!BIN)  // (a binned layout also depends on the bins: searched every call)
+      for (const auto& c : cache)
+        if (c[0] == H && c[1] == W && c[2] == lay.stages) groups = c[3];
     if (!groups) {
       // Most consumer threads resident per SM (measured to be what the
       // shading throughput tracks -- tools/sweep_rgb.py); ties go to the
@@ -536,7 +586,7 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
       const int gmax = std::max(1, std::min(kMaxCons / QW, (H + RPT - 1) / RPT));
       for (int g = 1; g <= gmax; ++g) {
         const Layout cand = with_groups(lay, g, W);
-        const size_t smem = cand.bytes(U8);
+        const size_t smem = need(cand);
         if (smem > kSmemPerSm) break;
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bulk_threads(W, g, FF), smem);
@@ -547,7 +597,7 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
         }
       }
       if (!groups) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: band ring does not fit in shared memory");
-      cache.push_back({H, W, lay.stages, groups});
+      if (!BIN) cache.push_back({H, W, lay.stages, groups});
     }
   }
   const int bulk_store = (W % 16 == 0) && ((reinterpret_cast<uintptr_t>(u8) & 15) == 0);
@@ -559,7 +609,8 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
   auto go = [&](int g, int ctas) -> int {
     const Layout l = with_groups(lay, g, W);
     const int threads = bulk_threads(W, g, FF);
-    const size_t smem = l.bytes(U8);
+    const size_t smem = need(l);
+    if (BIN) B.tab_ybins = use_tab ? band_ybins(H, l.band, B.bins_y) : 0;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (per_sm <= 0) return -1;
@@ -659,7 +710,7 @@ int dispatch(const float* depth, int64_t n, int H, int W, uint8_t* u8, float* f3
 int launch_rgb_binned(const float2* pairs, int bins_y, int bins_x, int degree, const float* depth, int64_t n,
                       int H, int W, uint8_t* u8, float* f32, cudaStream_t s) {
   LutParams L{};  // rep 0 ("color") float epilogue; coefficients come from the table
-  const BinArgs B{pairs, bins_y, bins_x};
+  const BinArgs B{pairs, bins_y, bins_x, 0};
   const Layout lay = base_layout(H, W, u8 != nullptr);
   auto go = [&](auto deg) -> int {
     constexpr int D = decltype(deg)::value;

@@ -154,3 +154,28 @@ def test_gpu_band_pipeline_binned_equals_simple_kernel(monkeypatch, deg, bins, n
     depth_to_rgb_binned_device(dd, v, out_u8=b, out_f32=fb)
     torch.cuda.synchronize()
     assert torch.equal(a, b) and torch.equal(fa, fb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("deg", [3, 4])
+def test_gpu_band_pipeline_table_in_smem_equals_l1(monkeypatch, deg):
+    """At degrees 3-4 the band pipeline reads its band's y bins from shared
+    memory; with TACSL_BINNED_L1 it reads the whole table through L1.  Same
+    FMA sequence, same bits (hundreds of images: CTAs keep their band)."""
+    import torch
+    from paper_2408_06506_b200.binned import depth_to_rgb_binned_device
+    size = (320, 240)
+    d, _ = _setup(size, n=6, cid=98)
+    d = np.ascontiguousarray(d[np.arange(300) % len(d)])
+    lut = synthetic.synthetic_lut(size, degree=deg, gradient_scale=synthetic.lut_scale(size))
+    v = vignetted_lut(lut, bins=(24, 32), falloff=0.3)
+    dd = torch.from_numpy(d).cuda()
+    a = torch.empty(dd.shape + (3,), dtype=torch.uint8, device="cuda")
+    fa = torch.empty(dd.shape + (3,), dtype=torch.float32, device="cuda")
+    depth_to_rgb_binned_device(dd, v, out_u8=a, out_f32=fa)
+    monkeypatch.setenv("TACSL_BINNED_L1", "1")
+    b = torch.empty_like(a)
+    fb = torch.empty_like(fa)
+    depth_to_rgb_binned_device(dd, v, out_u8=b, out_f32=fb)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(fa, fb)

@@ -47,7 +47,7 @@ def run(name, fn):
 
 run("K1 global LUT", lambda: depth_to_rgb_device(d, lut, out_u8=u8))
 for tag, b in (("6x8", b1), ("24x32", b2)):
-    for mode in ("", "TACSL_BINNED_BAND", "TACSL_BINNED_SIMPLE"):
+    for mode in ("", "TACSL_BINNED_BAND", "TACSL_BINNED_SIMPLE") + (("TACSL_BINNED_L1",) if DEG > 2 else ()):
         if mode:
             os.environ[mode] = "1"
         run(f"K6 binned {tag} {mode or 'dispatch'}", lambda: depth_to_rgb_binned_device(d, b, out_u8=u8))

@@ -103,12 +103,14 @@ TACSL_API int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n_
  * (y*bins_y/H, x*bins_x/W) (integer floor).  coeffs: HOST
  * (bins_y, bins_x, 3, n_terms) float64 in monomial_exponents order; the
  * table is uploaded to `device`.  INVALID_ARGUMENT for a degree outside
- * [2,4], bins outside [1, image size] or a table larger than shared memory. */
+ * [2,4] or bins outside [1, image size]. */
 TACSL_API int tacsl_binned_lut_create(int device, const double* coeffs, int degree, int bins_y,
                                       int bins_x, int width, int height, tacsl_binned_lut_t* out);
 TACSL_API void tacsl_binned_lut_destroy(tacsl_binned_lut_t lut);
 
-/* tacsl_depth_to_rgb through a binned LUT (same layouts, outputs and errors). */
+/* tacsl_depth_to_rgb through a binned LUT (same layouts, outputs and errors).
+ * Tables over 96 KB (float32) additionally need width % 4 == 0, 16-B aligned
+ * buffers and every x-bin edge on an even column, else INVALID_ARGUMENT. */
 TACSL_API int tacsl_depth_to_rgb_binned(tacsl_binned_lut_t lut, const float* depth, int64_t n_images,
                                         int height, int width, uint8_t* rgb_u8, float* rgb_f32,
                                         void* stream);

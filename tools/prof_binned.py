@@ -1,5 +1,8 @@
 """One K6 launch per bin shape (6x8, 24x32) at 2048 x 240x320, for
-`ncu --set full -k regex:rgb_bulk_kernel` (both go through the band pipeline)."""
+`ncu --set full -k regex:rgb_bulk_kernel` (both go through the band pipeline
+at degree 2; at degree 3 only 24x32 does).
+
+    python tools/prof_binned.py [frames] [degree]"""
 import sys
 from pathlib import Path
 
@@ -10,7 +13,8 @@ from paper_2408_06506_b200 import synthetic  # noqa: E402
 from paper_2408_06506_b200.binned import depth_to_rgb_binned_device, device_binned_lut, vignetted_lut  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
-_, cam, bg, lut, _ = synthetic.sensor_setup((320, 240))
+DEG = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+_, cam, bg, lut, _ = synthetic.sensor_setup((320, 240), lut_degree=DEG)
 pool = torch.from_numpy(synthetic.depth_batch(cam, bg, 64)).cuda()
 d = pool[torch.arange(N, device="cuda") % 64].contiguous()
 u8 = torch.empty(d.shape + (3,), dtype=torch.uint8, device="cuda")

@@ -217,3 +217,26 @@ def test_env_render_params_shapes_and_errors(env):
         env_render_params_device(env["sdf"], torch.zeros((3, 20), dtype=torch.float64, device="cuda"), 2)
     with pytest.raises(ValueError):
         env_render_params_device(env["sdf"], torch.zeros((3, 21), dtype=torch.float32, device="cuda"), 2)
+
+
+@pytest.mark.parametrize("rep", ["color", "diff", "concat"])
+def test_batched_env_images_without_augmentation(env, rep):
+    """envs.tactile_images with augmentation off, in each representation
+    (envs/peg_tasks.py:445-458): the reference env's recorded depth maps
+    shaded by the CPU restatement, cast to float32, then "diff" subtracts
+    and "concat" appends the LUT's background colour."""
+    from oracle import gelsim_oracle as O
+    from paper_2408_06506_b200 import envs
+    e = _standin_env(env, None)
+    e.cfg.tactile_rep = rep
+    got = envs.tactile_images(e)
+    rgb = O.depth_to_rgb(env["depth"], env["lut_coeffs"], int(env["lut_degree"])).astype(np.float32)
+    nominal = env["lut_coeffs"][:, 0].astype(np.float32)
+    if rep == "diff":
+        ref = rgb - nominal
+    elif rep == "concat":
+        ref = np.concatenate([rgb, np.broadcast_to(nominal, rgb.shape)], axis=-1)
+    else:
+        ref = rgb
+    assert got.dtype == np.float32 and got.shape == ref.shape
+    np.testing.assert_allclose(got, ref, rtol=0, atol=2e-6)

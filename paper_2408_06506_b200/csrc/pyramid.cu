@@ -403,13 +403,20 @@ template <int R, int S>
 int dispatch_bulk(const float* in, int64_t n, int H, int W, int Ho, int Wo, const Taps& T, float* out,
                   cudaStream_t stream) {
   static std::mutex mu;
-  static std::vector<std::array<int, 6>> cache;  // (H, W) -> (rpt, groups, stages)
+  static std::vector<std::array<int, 6>> cache;  // (H, W, log2 n) -> (rpt, groups, stages)
+  auto launch = [&](const FLayout& l) -> int {
+    if constexpr (R <= 4) {
+      if (l.rpt == 8) return launch_bulk_filter<R, S, 8>(in, n, H, W, Ho, Wo, T, out, stream, l);
+    }
+    return launch_bulk_filter<R, S, 4>(in, n, H, W, Ho, Wo, T, out, stream, l);
+  };
+  const int nb = 63 - __builtin_clzll((unsigned long long)std::max<int64_t>(n, 1));
   FLayout best;
   {
     std::lock_guard<std::mutex> lock(mu);
     bool found = false;
     for (const auto& c : cache)
-      if (c[0] == H && c[1] == W) {
+      if (c[0] == H && c[1] == W && c[2] == nb) {
         best.rpt = c[3];
         best.groups = c[4];
         best.stages = c[5];
@@ -421,6 +428,7 @@ int dispatch_bulk(const float* in, int64_t n, int H, int W, int Ho, int Wo, cons
       const int want_groups = env_int_f("TACSL_FILTER_GROUPS", 0);
       const int stages = std::min(env_int_f("TACSL_FILTER_STAGES", 2), kFMaxStages);
       long best_score = -1;
+      std::vector<FLayout> cands;  // the deepest ring that fits per (rpt, groups), two stages or more
       for (int rpt : {8, 4}) {
         if ((want_rpt && rpt != want_rpt) || (rpt == 8 && R > 4)) continue;  // RPT=8 spills beyond R=4
         const int gmax = std::max(1, std::min(kFMaxCons / QW, (Ho + rpt - 1) / rpt));
@@ -441,6 +449,7 @@ int dispatch_bulk(const float* in, int64_t n, int H, int W, int Ho, int Wo, cons
             // a single stage cannot overlap the next band's load with this
             // one's filtering: only a last resort
             if (st < 2) sc = 1;
+            else cands.push_back(cand);
             // strictly better occupancy wins; on a tie the taller band
             if (sc > best_score || (sc == best_score && cand.band() > best.band())) {
               best_score = sc;
@@ -451,13 +460,39 @@ int dispatch_bulk(const float* in, int64_t n, int H, int W, int Ho, int Wo, cons
         }
       }
       if (best_score <= 0) return -1;  // caller falls back to the generic kernel
-      cache.push_back({H, W, 0, best.rpt, best.groups, best.stages});
+      // The occupancy score misses part of what the measured best layout
+      // depends on (pyr_down at 2048 x 480x640: 0.575 ms scored vs 0.539 ms
+      // for 2 groups x 4 rows), so the first un-captured call per (H, W,
+      // batch-size octave) times the candidates on its own data.
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(stream, &cap);
+      if (cands.size() > 1 && !want_rpt && !want_groups && cap == cudaStreamCaptureStatusNone &&
+          !std::getenv("TACSL_FILTER_NO_TUNE")) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float best_ms = 1e30f;
+        for (const FLayout& c : cands) {
+          if (launch(c)) continue;  // warm-up
+          cudaEventRecord(e0, stream);
+          launch(c);
+          launch(c);
+          cudaEventRecord(e1, stream);
+          cudaEventSynchronize(e1);
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best_ms) {
+            best_ms = ms;
+            best = c;
+          }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
+      cache.push_back({H, W, nb, best.rpt, best.groups, best.stages});
     }
   }
-  if constexpr (R <= 4) {
-    if (best.rpt == 8) return launch_bulk_filter<R, S, 8>(in, n, H, W, Ho, Wo, T, out, stream, best);
-  }
-  return launch_bulk_filter<R, S, 4>(in, n, H, W, Ho, Wo, T, out, stream, best);
+  return launch(best);
 }
 
 template <int S>

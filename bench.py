@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     p.add_argument("--e2e-chunks", type=int, default=64, help="env chunks pipelined over H2D / compute / D2H")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample length")
+    p.add_argument("--sustain-s", type=float, default=1.5,
+                   help="seconds of back-to-back steps for value_sustained (0: skip)")
     p.add_argument("--envs", type=int, default=None,
                    help="override the config's env count (experiments, e.g. one GPU's share at N GPUs)")
     return p.parse_args()
@@ -206,6 +208,223 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------- ours ---
 
+class Ctx:
+    """One rank's share of a benchmark workload, resident on its GPU."""
+
+
+def setup_workload(wl, rank, world, dev, fused=False, overlap=True):
+    """Build this rank's env shard of config `wl` exactly as the timed step
+    runs it: device-resident inputs (global frame g uses indenter map g % 64
+    and the states of env g // S, whatever the rank count) and the
+    SensorArray (fp32 force outputs, uint8 RGB)."""
+    import torch
+
+    from paper_2408_06506_b200 import SensorArray, synthetic
+    from paper_2408_06506_b200.pipeline import shard_range
+    from paper_2408_06506_b200.tactile import PenaltyParams
+
+    c = Ctx()
+    c.wl = wl
+    c.lo, c.hi = shard_range(wl.n_envs, rank, world)
+    E, S = c.hi - c.lo, wl.n_sensors
+    W, H = wl.image_size
+    c.E, c.S, c.H, c.W = E, S, H, W
+    _, c.cam, c.bg, c.lut, c.pts = synthetic.sensor_setup(wl.image_size, wl.ff_grid, lut_degree=wl.lut_degree)
+    c.sdf = synthetic.peg_grid(wl.sdf_dims)
+    c.params = PenaltyParams()
+    c.pool = synthetic.depth_batch(c.cam, c.bg, 64, config_id=wl.config_id)
+    pool = torch.from_numpy(c.pool).to(dev)
+    idx = (torch.arange(E * S, device=dev) + c.lo * S) % pool.shape[0]  # this shard's slice of the global job
+    c.depth = pool[idx].reshape(E, S, H, W).contiguous()
+    del pool, idx
+    c.obj_all, c.sen_all = synthetic.peg_states(wl.n_envs, S, config_id=wl.config_id)
+    c.obj = torch.from_numpy(c.obj_all[c.lo:c.hi]).to(dev)
+    c.sen = torch.from_numpy(np.ascontiguousarray(c.sen_all[c.lo:c.hi])).to(dev)
+    c.arr = SensorArray(c.lut, c.sdf, c.pts, c.params, E, S, device=dev, overlap=overlap, rgb_u8=wl.rgb,
+                        with_ff=wl.ff, fused=fused, pyramid_levels=wl.pyramid_levels,
+                        smooth_sigma=wl.smooth_sigma)
+    return c
+
+
+def sample_indices(frames, n=16):
+    """Deterministic global frame indices checked against the oracle: both
+    ends, the middle, the first/last frame of every eighth of the job (rank
+    boundaries at N = 1, 2, 4, 8) and seeded random picks."""
+    idx = {0, frames - 1, frames // 2}
+    for k in range(1, 8):
+        b = k * frames // 8
+        idx.update((b - 1, b))
+    rng = np.random.default_rng(20240812)
+    extra = [int(i) for i in rng.integers(0, frames, 4 * n)]
+    for i in extra:
+        if len(idx) >= n:
+            break
+        idx.add(i)
+    return np.array(sorted(i for i in idx if 0 <= i < frames), dtype=np.int64)
+
+
+def gather_rows(outputs, owned, n_rows, world, coll_dev):
+    """All-gather sampled per-frame rows to every rank (rank 0 uses them).
+
+    outputs: list of (name, (n_local_frames, ...) device tensor); owned: list
+    of (row in the sample, local frame index) this rank holds.  Each rank
+    sends an (n_rows, frame bytes) uint8 block with its own rows filled
+    (zeros elsewhere) over the process group (NCCL on the GPU box, gloo in
+    the CPU tests); the result maps name -> (n_rows, frame bytes) uint8 numpy
+    with every row taken from the rank that owns it."""
+    import torch
+    import torch.distributed as dist
+
+    out = {}
+    for name, x in outputs:
+        flat = x.reshape(x.shape[0], -1)
+        nb = flat.shape[1] * flat.element_size()
+        block = torch.zeros((n_rows, nb), dtype=torch.uint8, device=x.device)
+        have = torch.zeros(n_rows, dtype=torch.uint8, device=x.device)
+        if owned:
+            rows = torch.tensor([r for r, _ in owned], device=x.device)
+            loc = torch.tensor([f for _, f in owned], device=x.device)
+            block[rows] = flat[loc].contiguous().view(torch.uint8).reshape(len(owned), nb)
+            have[rows] = 1
+        block, have = block.to(coll_dev), have.to(coll_dev)
+        if world > 1:
+            parts = [torch.empty_like(block) for _ in range(world)]
+            hv = [torch.empty_like(have) for _ in range(world)]
+            dist.all_gather(parts, block)
+            dist.all_gather(hv, have)
+            owner = torch.stack(hv).to(torch.int64).argmax(dim=0)  # the rank that holds each row
+            block = torch.stack(parts)[owner, torch.arange(n_rows, device=block.device)]
+        out[name] = (block.cpu().numpy(), np.dtype(str(x.dtype).replace("torch.", "")), tuple(x.shape[1:]))
+    return {k: b.view(dt).reshape((n_rows,) + shp) for k, (b, dt, shp) in out.items()}
+
+
+def gather_digests(digests, n_local, world, coll_dev):
+    """Concatenate every rank's (n_local, k) int64 frame digests in rank
+    (= global env) order; returns the (frames, k) numpy array on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    d = digests.to(coll_dev)
+    if world == 1:
+        return d.cpu().numpy()
+    n = torch.tensor([n_local], dtype=torch.int64, device=coll_dev)
+    ns = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(ns, n)
+    counts = [int(v.item()) for v in ns]
+    pad = torch.zeros((max(counts), d.shape[1]), dtype=d.dtype, device=coll_dev)
+    pad[:n_local] = d
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    return np.concatenate([p[:c].cpu().numpy() for p, c in zip(parts, counts)])
+
+
+def digest_summary(names, table):
+    """sha256 over the per-frame digest table (frame order, little endian),
+    whole and per output -- independent of the rank count."""
+    import hashlib
+
+    tab = np.ascontiguousarray(table.astype("<i8"))
+    return {"sha256": hashlib.sha256(tab.tobytes()).hexdigest(),
+            "per_output": {n: hashlib.sha256(np.ascontiguousarray(tab[:, j]).tobytes()).hexdigest()[:16]
+                           for j, n in enumerate(names)},
+            "frames": int(tab.shape[0]),
+            "rule": "per-frame tacsl_frame_digest of every output, concatenated over ranks in env order"}
+
+
+def check_parity(c, idx, got):
+    """Rank 0: the oracle (numpy restatement of gelsim, pinned to the
+    reference's golden vectors) on the sampled frames' inputs, regenerated
+    from the same seeds, against the gathered device outputs."""
+    from oracle import gelsim_oracle as O
+
+    wl = c.wl
+    S = wl.n_sensors
+    res = {"frames_checked": [int(i) for i in idx]}
+    env, sensor = idx // S, idx % S
+    ok = True
+    if wl.rgb:
+        depth = c.pool[idx % len(c.pool)].astype(np.float64)
+        if wl.pyramid_levels > 1 or wl.smooth_sigma > 0:
+            from oracle.pyramid_oracle import separable_filter
+            from paper_2408_06506_b200 import smoothing
+            x = separable_filter(depth, smoothing.gaussian_taps(wl.smooth_sigma), 1) if wl.smooth_sigma else depth
+            refs = []
+            for lvl in range(wl.pyramid_levels):
+                if lvl:
+                    x = separable_filter(x, smoothing.BINOMIAL5, 2)
+                ll = smoothing.level_lut(c.lut, lvl)
+                refs.append(("rgb" if lvl == 0 else f"rgb_l{lvl}", O.to_uint8(O.depth_to_rgb(x, ll.coeffs, ll.degree))))
+            frac_tol = 2e-2  # fp32 chain vs the float64 restatement (tests/test_pyramid.py)
+        else:
+            refs = [("rgb", O.to_uint8(O.depth_to_rgb(depth, c.lut.coeffs, c.lut.degree)))]
+            frac_tol = 1e-4  # fp32 polynomial vs the float64 reference (SURVEY.md 8c)
+        lsb, off, n = 0, 0, 0
+        for name, ref in refs:
+            d = np.abs(got[name].astype(np.int64) - ref.astype(np.int64))
+            lsb = max(lsb, int(d.max()))
+            off += int((d > 0).sum())
+            n += d.size
+        res.update(rgb_max_lsb=lsb, rgb_frac_off=off / n, rgb_values_checked=n, rgb_frac_tol=frac_tol)
+        ok &= lsb <= 1 and off / n <= frac_tol
+    if wl.ff:
+        o = c.obj_all[env]
+        s = c.sen_all[env, sensor]
+        sdf = (c.sdf.origin, c.sdf.spacing, c.sdf.dims, c.sdf.values, c.sdf.gradients)
+        f_n, f_t, _ = O.compute_force_field(c.pts.points, *sdf, o[:, 0:3], o[:, 3:7], o[:, 7:10], o[:, 10:13],
+                                            s[:, 0:3], s[:, 3:7], s[:, 7:10], s[:, 10:13],
+                                            c.params.k_n, c.params.k_d, c.params.k_t, c.params.mu)
+        force, torque = O.net_wrench(f_n, f_t, c.pts.points)
+        worst, zero_abs, mism = 0.0, 0.0, 0
+        for g, r in ((got["f_n"], f_n), (got["f_t"], f_t)):
+            g = g.astype(np.float64)
+            err = np.linalg.norm(g - r, axis=-1)
+            nr = np.linalg.norm(r, axis=-1)
+            nz = nr > 0
+            if nz.any():
+                worst = max(worst, float((err[nz] / nr[nz]).max()))
+            if (~nz).any():
+                zero_abs = max(zero_abs, float(err[~nz].max()))
+        gm = (np.abs(got["f_n"]).sum(-1) + np.abs(got["f_t"]).sum(-1)) > 0
+        rm = (np.abs(f_n).sum(-1) + np.abs(f_t).sum(-1)) > 0
+        mism = int((gm != rm).sum())
+        w = got["wrench"]
+        ref_w = np.concatenate([force, torque], axis=-1)
+        scale = np.abs(f_n).sum(axis=(-3, -2, -1)) + np.abs(f_t).sum(axis=(-3, -2, -1)) + 1e-30
+        w_rel = float((np.abs(w - ref_w).max(axis=-1) / scale).max())
+        res.update(ff_max_rel=worst, ff_max_abs_where_ref_zero=zero_abs, mask_mismatches=mism,
+                   contact_taxels=int(rm.sum()), taxels_checked=int(rm.size), wrench_max_rel_of_sum_abs_f=w_rel)
+        ok &= worst <= 1e-5 and zero_abs <= 1e-9 and mism == 0 and w_rel <= 1e-6
+    res["ok"] = bool(ok)
+    res["rule"] = ("sampled frames of the last timed step vs the oracle on the same inputs: RGB <= 1 LSB "
+                   "(fraction of values off by one <= rgb_frac_tol), forces <= 1e-5 relative per taxel, "
+                   "identical nonzero-force (contact) masks, wrench <= 1e-6 of sum |f|")
+    return res
+
+
+def validate(c, world, rank, coll_dev, n_samples=16):
+    """Outside every timed region: sampled-frame oracle parity of the last
+    step (gathered to rank 0 over the process group) and the whole-job
+    per-frame digest table (gathered the same way)."""
+    import torch
+
+    arr = c.arr
+    S = c.wl.n_sensors
+    names, dig = arr.frame_digests()
+    table = gather_digests(dig, c.E * S, world, coll_dev)
+    idx = sample_indices(c.wl.frames, n_samples)
+    owned = [(r, int(g) - c.lo * S) for r, g in enumerate(idx) if c.lo * S <= g < c.hi * S]
+    outs = []
+    for name, x in arr.outputs():
+        if name == "rgb_f32":
+            continue
+        outs.append((name, x.reshape((c.E * S,) + tuple(x.shape[2:]))))
+    got = gather_rows(outs, owned, len(idx), world, coll_dev)
+    torch.cuda.synchronize()
+    if rank != 0:
+        return None
+    return {"parity": check_parity(c, idx, got), "digest": digest_summary(names, table)}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -213,9 +432,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2408_06506_b200 import SensorArray, synthetic
-    from paper_2408_06506_b200.pipeline import shard_range
-    from paper_2408_06506_b200.tactile import PenaltyParams
+    from paper_2408_06506_b200 import synthetic
 
     rank, world, local = dist_env()
     # one process per GPU; TACSL_DIST_BACKEND=gloo lets a multi-rank run share
@@ -246,25 +463,9 @@ def main():
     if args.envs:
         import dataclasses
         wl = dataclasses.replace(wl, n_envs=args.envs)
-    lo, hi = shard_range(wl.n_envs, rank, world)
-    E, S = hi - lo, wl.n_sensors
-    W, H = wl.image_size
-    _, cam, bg, lut, pts = synthetic.sensor_setup(wl.image_size, wl.ff_grid, lut_degree=wl.lut_degree)
-    sdf = synthetic.peg_grid(wl.sdf_dims)
-    params = PenaltyParams()
+    c = setup_workload(wl, rank, world, dev, fused=args.fused, overlap=not args.no_overlap)
+    arr, depth, obj, sen = c.arr, c.depth, c.obj, c.sen
 
-    # ---- inputs resident in HBM: 64 distinct indenter maps tiled to E*S frames
-    pool = torch.from_numpy(synthetic.depth_batch(cam, bg, 64, config_id=wl.config_id)).to(dev)
-    idx = (torch.arange(E * S, device=dev) + lo * S) % pool.shape[0]  # this shard's slice of the global job
-    depth = pool[idx].reshape(E, S, H, W).contiguous()
-    del pool, idx
-    obj_all, sen_all = synthetic.peg_states(wl.n_envs, S, config_id=wl.config_id)
-    obj = torch.from_numpy(obj_all[lo:hi]).to(dev)
-    sen = torch.from_numpy(np.ascontiguousarray(sen_all[lo:hi])).to(dev)
-
-    arr = SensorArray(lut, sdf, pts, params, E, S, device=dev, overlap=not args.no_overlap, rgb_u8=wl.rgb,
-                      with_ff=wl.ff, fused=args.fused, pyramid_levels=wl.pyramid_levels,
-                      smooth_sigma=wl.smooth_sigma)
     use_graph = not args.no_graph
     if use_graph:
         arr.capture(depth, obj, sen)
@@ -303,19 +504,42 @@ def main():
         torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream(dev)
-    clocks = ClockSampler(local)
-    with clocks:
+
+    def timed_steps(n):
         barrier()
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(n):
             step()
         t1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ms_local = t0.elapsed_time(t1)
+        return t0.elapsed_time(t1)
+
+    clocks = ClockSampler(local)
+    with clocks:
+        ms_local = timed_steps(args.steps)
+    ms = max_over_ranks(ms_local)
+    ms_per_step = ms / args.steps
+    frames_total = wl.frames  # all ranks together
+    value = frames_total / (ms_per_step / 1e3)
+
+    # ---- validation of the last timed step (outside every timed region)
+    validation = validate(c, world, rank, coll_dev)
+
+    # ---- sustained: back-to-back steps for >= --sustain-s seconds (RL
+    # training steps continuously; the board power limiter then lowers the
+    # SM clock), with its own clock record
+    sustained = None
+    if args.sustain_s > 0:
+        n_sus = max(args.steps, int(np.ceil(args.sustain_s / max(ms_per_step / 1e3, 1e-6))))
+        sclk = ClockSampler(local)
+        with sclk:
+            ms_sus = max_over_ranks(timed_steps(n_sus))
+        sustained = {"value": frames_total / (ms_sus / n_sus / 1e3), "ms_per_step": ms_sus / n_sus,
+                     "steps": n_sus, "seconds": ms_sus / 1e3, "clocks": sclk.summary()}
 
     # ---- per-kernel durations (each kernel's own graph, replayed on the
     # current stream -- the stream its launches were captured from)
@@ -352,10 +576,6 @@ def main():
             step()
         k1_sus = time_kernel(k1_fn, nk, 3) if wl.rgb else None
         k2_sus = time_kernel(k2_fn, nk, 3) if wl.ff else None
-    ms = max_over_ranks(ms_local)
-    ms_per_step = ms / args.steps
-    frames_total = wl.frames  # all ranks together
-    value = frames_total / (ms_per_step / 1e3)
 
     # ---- end to end through the host-buffer API
     def measure_e2e():
@@ -398,16 +618,6 @@ def main():
 
     e2e = None if args.no_e2e else measure_e2e()
 
-    # ---- validation digest across ranks (outside every timed region)
-    from paper_2408_06506_b200.pipeline import frame_checksum
-    dig = frame_checksum(arr.rgb_u8, arr.f_n, arr.f_t).to(coll_dev)  # None-safe
-    if world > 1:
-        parts = [torch.zeros_like(dig) for _ in range(world)]
-        dist.all_gather(parts, dig)
-        dig = torch.stack(parts).sum(dim=0)
-    validation = {"digest": [float(v) for v in dig.cpu()],
-                  "rule": "sum over ranks of (sum RGB bytes, sum |f_n|, sum |f_t|) of the last step's outputs"}
-
     # ---- roofline of the dominant kernel (K1, or K2 when the step has no RGB) and of the whole step
     peak, peak_src = hbm_peak()
     bytes_ = arr.algorithmic_bytes()
@@ -422,11 +632,10 @@ def main():
         kname, kms, kbytes = "rgb_bulk_kernel", k1_ms, bytes_["rgb"]
         desc, rule = "rgb_bulk_kernel (K1 depth->RGB)", "7 B/px: 4 B fp32 depth read + 3 B uint8 RGB written"
     elif wl.rgb:
-        kname, kms, kbytes = "image_pipeline", k1_ms, bytes_["rgb"]
-        desc = ("image pipeline: sep_bulk_kernel smoothing + rgb_bulk_kernel, then per pyramid level "
-                "sep_bulk_kernel pyr_down + rgb_bulk_kernel (all launches of the RGB side)")
-        rule = ("smoothing 8 B/px + K1 7 B/px at level 0; per level l>=1: pyr_down 20 B per output px + "
-                "K1 7 B/px")
+        kname, kms, kbytes = arr.image_kernel_name(), k1_ms, bytes_["rgb"]
+        desc = arr.image_kernel_desc()
+        rule = ("SURVEY.md 8d: 4 B fp32 depth read per level-0 pixel + 3 B uint8 RGB written per pixel of "
+                "every pyramid level (intermediates are not algorithmic bytes)")
     else:
         kname, kms, kbytes = "force_field_fast_kernel", k2_ms, bytes_["ff"]
         desc = ("force_field_fast_kernel (K2 force field + wrench; float64 / L2-gather-latency bound, "
@@ -442,6 +651,8 @@ def main():
         "data": "synthetic (analytic spherical-indenter depth maps, analytic peg SDF, random peg poses)",
         "config": workload_config(wl, world),
         "e2e": e2e,
+        "value_sustained": sustained["value"] if sustained else None,
+        "sustained": sustained,
         "roofline": {"bound": "hbm", "kernel": desc, "achieved": k_gbs,
                      "peak": peak, "unit": "GB/s", "frac": k_gbs / peak, "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kms,
@@ -459,9 +670,12 @@ def main():
                                    "after_steps": max(args.steps, 400), "clocks": sclocks.summary()}},
         "gpu_launches": arr.launches_per_step * args.steps,
         "clocks": clocks.summary(),
-        "graph": use_graph, "fused": arr.fused, "overlap": arr.overlap, "validation": validation,
+        "graph": use_graph, "fused": arr.fused, "overlap": arr.overlap,
         "settle_s": args.settle,
     }
+    if validation is not None:
+        line["parity"] = validation["parity"]
+        line["validation"] = validation["digest"]
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle.cpu_bench import CpuBaseline, cpu_model

@@ -14,7 +14,12 @@
  *                           lut.py:56-65, and to_uint8 render/imageio.py:8-11
  *                           fused as the uint8 epilogue)
  *   tacsl_lut_create        render/lut.py:31-54   PolyLut (coefficients + image_size)
- *   tacsl_to_uint8          render/imageio.py:8-11 to_uint8 (standalone)
+ *   tacsl_to_uint8          render/imageio.py:8-11 to_uint8 (standalone, float32 input)
+ *   tacsl_to_uint8_f64      render/imageio.py:8-11 to_uint8 on float64 input, in float64
+ *   tacsl_f64_to_f32 /      the numpy drop-ins' dtype changes (the reference computes in
+ *   tacsl_f32_to_f64        float64; np.asarray(..., float64) / astype) done on the device
+ *   tacsl_frame_digest      (no reference counterpart) per-frame 64-bit digests of a
+ *                           step's outputs for cross-rank validation
  *   tacsl_sdf_create        geometry/sdf.py:29-54 SdfGrid (device upload)
  *   tacsl_query_sdf         geometry/sdf.py:271-321 query_sdf
  *   tacsl_penalty_forces    tactile/field.py:61-76 penalty_forces
@@ -24,6 +29,8 @@
  *   tacsl_net_wrench        tactile/field.py:132-141 net_wrench (standalone)
  *   tacsl_render_depth      render/depth.py:88-134 render_depth (SDF sphere tracer)
  *   tacsl_env_render_params envs/peg_tasks.py:440-442 + render/depth.py:105-121 (per-env render inputs)
+ *   tacsl_rgb_pyramid       render/lut.py:68-76 extended (no reference counterpart, SURVEY.md 8a
+ *                           a13): Gaussian smoothing + tactile RGB of a 1-3 level pyramid in one pass
  *
  * The reference has no FFI of its own (pure numpy); the Python module
  * paper_2408_06506_b200 binds these with ctypes behind the reference's
@@ -169,6 +176,26 @@ TACSL_API int tacsl_separable_filter(const float* in, int64_t n_images, int heig
 /* x (count) float32 -> u8 = clip(rint(255*x), 0, 255) (imageio.py:8-11). */
 TACSL_API int tacsl_to_uint8(const float* x, int64_t count, uint8_t* out, void* stream);
 
+/* x (count) float64 -> u8 = clip(rint(x*255), 0, 255) computed in float64
+ * exactly as imageio.py:8-11 (product rounded to float64, ties to even;
+ * NaN -> 0). */
+TACSL_API int tacsl_to_uint8_f64(const double* x, int64_t count, uint8_t* out, void* stream);
+
+/* Element-wise dtype conversion on the device (round to nearest even, as
+ * numpy's astype): the float64 arrays the reference's callers pass in are
+ * uploaded as they are and narrowed here; float32 results are widened here
+ * before one device->host copy. */
+TACSL_API int tacsl_f64_to_f32(const double* x, int64_t count, float* out, void* stream);
+TACSL_API int tacsl_f32_to_f64(const float* x, int64_t count, double* out, void* stream);
+
+/* out[f] = 64-bit digest of frame f = data[f*frame_bytes, (f+1)*frame_bytes):
+ * sum over the frame's 32-bit words w_i of splitmix64((i << 32) | w_i),
+ * mod 2^64, finalised with the word count.  Position-dependent (swapped
+ * channels, shifted rows and misplaced frames change it) and independent of
+ * how the frames are sharded.  frame_bytes % 4 == 0, data 4-B aligned. */
+TACSL_API int tacsl_frame_digest(const void* data, int64_t n_frames, int64_t frame_bytes, uint64_t* out,
+                                 void* stream);
+
 /* ---------------------------------------------------------------- SDF --- */
 /* values: HOST (nx,ny,nz) float64, gradients: HOST (nx,ny,nz,3) float64,
  * z fastest (sdf.py:29-41).  Uploaded as a float64 {d, gx, gy, gz} cell grid
@@ -264,6 +291,25 @@ TACSL_API int tacsl_sensor_step(tacsl_lut_t lut, const float* depth, int64_t n_i
                                 int64_t sensor_stride, int64_t n_envs, int n_sensors,
                                 tacsl_penalty_t params, float* f_n, float* f_t, double* wrench,
                                 unsigned long long* workspace, void* stream);
+
+/* Smoothed multi-scale tactile RGB in ONE pass over the depth maps (the
+ * config-5 image chain; no reference counterpart -- the stage extends
+ * render/lut.py:68-76).  For each of n_images (height, width) float32
+ * depth maps: smooth with the separable (2*radius+1)-tap filter `taps`
+ * (HOST floats; 'nearest' borders; radius 0 = no smoothing), then level 0
+ * = tacsl_depth_to_rgb of the smoothed map with luts[0], and level l >= 1 =
+ * tacsl_depth_to_rgb of the 5-tap binomial [1,4,6,4,1]/16 decimation of
+ * level l-1 (even rows/columns) with luts[l] (image_size (W >> l, H >> l)).
+ * out[l]: (n, H >> l, W >> l, 3) uint8.  Bit-identical to running
+ * tacsl_separable_filter and tacsl_depth_to_rgb level by level, with only
+ * the depth read and the RGB written to memory.  Requires
+ * tacsl_rgb_pyramid_supported(height, width, radius, levels) (levels 1-3,
+ * radius 0-4, width % 4 == 0 and <= 1024, height % 4 == 0) else
+ * INVALID_ARGUMENT; LUT size mismatch -> LUT_RESOLUTION_MISMATCH. */
+TACSL_API int tacsl_rgb_pyramid_supported(int height, int width, int radius, int levels);
+TACSL_API int tacsl_rgb_pyramid(const tacsl_lut_t* luts, int levels, const float* depth, int64_t n_images,
+                                int height, int width, const float* taps, int radius, uint8_t* const* out,
+                                void* stream);
 
 /* net_wrench on an existing field: f_n, f_t (frames, rows, cols, 3) float64,
  * points (rows, cols, 3) float64 -> force, torque (frames, 3) float64. */

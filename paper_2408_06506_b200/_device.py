@@ -64,3 +64,33 @@ def stream_handle(device) -> int:
 
 def ptr(x) -> int | None:
     return None if x is None else x.data_ptr()
+
+
+def as_f32(x, device):
+    """numpy / torch float data -> contiguous float32 CUDA tensor on `device`.
+    float64 input is uploaded as it is and narrowed ON THE DEVICE
+    (tacsl_f64_to_f32, numpy's astype rounding), so the host never touches
+    the values; other dtypes take the plain path."""
+    t = torch()
+    if isinstance(x, t.Tensor):
+        if x.dtype == t.float32:
+            return x.to(device=device).contiguous()
+        if x.dtype != t.float64:
+            return x.to(device=device, dtype=t.float32).contiguous()
+        src = x.to(device=device).contiguous()
+    else:
+        arr = np.asarray(x)
+        if arr.dtype != np.float64:
+            return to_device(arr, t.float32, device)
+        src = to_device(arr, t.float64, device)
+    out = t.empty(src.shape, dtype=t.float32, device=device)
+    _lib.check(_lib.load().tacsl_f64_to_f32(src.data_ptr(), src.numel(), out.data_ptr(), stream_handle(device)))
+    return out
+
+
+def widen_f64(x):
+    """float32 CUDA tensor -> float64 CUDA tensor (tacsl_f32_to_f64)."""
+    t = torch()
+    out = t.empty(x.shape, dtype=t.float64, device=x.device)
+    _lib.check(_lib.load().tacsl_f32_to_f64(x.data_ptr(), x.numel(), out.data_ptr(), stream_handle(x.device)))
+    return out

@@ -40,6 +40,12 @@ SIGNATURES = {
     "tacsl_lut_destroy": (None, [c_void_p]),
     "tacsl_depth_to_rgb": (c_int, [c_void_p, P, c_int64, c_int, c_int, P, P, c_void_p]),
     "tacsl_to_uint8": (c_int, [P, c_int64, P, c_void_p]),
+    "tacsl_to_uint8_f64": (c_int, [P, c_int64, P, c_void_p]),
+    "tacsl_f64_to_f32": (c_int, [P, c_int64, P, c_void_p]),
+    "tacsl_f32_to_f64": (c_int, [P, c_int64, P, c_void_p]),
+    "tacsl_frame_digest": (c_int, [P, c_int64, c_int64, P, c_void_p]),
+    "tacsl_rgb_pyramid_supported": (c_int, [c_int, c_int, c_int, c_int]),
+    "tacsl_rgb_pyramid": (c_int, [P, c_int, P, c_int64, c_int, c_int, P, c_int, P, c_void_p]),
     "tacsl_sdf_create": (c_int, [c_int, P, P, P, P, c_double, ctypes.POINTER(c_void_p)]),
     "tacsl_sdf_destroy": (None, [c_void_p]),
     "tacsl_query_sdf": (c_int, [c_void_p, P, c_int64, P, P, P, c_void_p]),

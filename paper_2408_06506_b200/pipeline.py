@@ -76,24 +76,30 @@ class SensorArray:
         self._graph_inputs = None
         assert F > 0
 
-    # bytes the step must move through HBM (our exact layout)
+    # bytes the step must move through HBM (our exact layout):
+    # the fp32 depth read once, every output byte written once; smoothed and
+    # decimated intermediates are not algorithmic bytes (a fused pipeline
+    # never writes them)
     def algorithmic_bytes(self) -> dict:
         px = self.H * self.W
         rgb_out = (3 if self.rgb_u8 is not None else 0) + (12 if self.rgb_f32 is not None else 0)
         F = self.E * self.S
         rgb = F * px * (4 + rgb_out) if self.with_rgb else 0
-        if self.with_rgb and self.sigma > 0:
-            rgb += F * px * 8  # smoothing: fp32 depth read + smoothed depth written
         for d in self._lvl_depth[1:]:
             h, w = d.shape[-2:]
-            # pyr_down reads the level above (4 px per output px) and writes fp32;
-            # K1 reads the level and writes uint8 RGB
-            rgb += F * h * w * (16 + 4) + F * h * w * 7
+            rgb += F * h * w * 3  # level l's uint8 RGB
         ff = 0
         if self.with_ff:
             taxel_out = self.rows * self.cols * 3 * self.f_n.element_size() * 2
             ff = F * (taxel_out + 13 * 8 + 6 * 8) + self.E * 13 * 8
         return {"rgb": rgb, "ff": ff, "total": rgb + ff}
+
+    def image_kernel_name(self) -> str:
+        return "image_pipeline"
+
+    def image_kernel_desc(self) -> str:
+        return ("image pipeline: sep_bulk_kernel smoothing + rgb_bulk_kernel, then per pyramid level "
+                "sep_bulk_kernel pyr_down + rgb_bulk_kernel (all launches of the RGB side)")
 
     def launch(self, depth, obj_state, sen_state):
         """Enqueue one step on the current stream (K2 on a forked stream that
@@ -187,11 +193,22 @@ class SensorArray:
         self._graph.replay()
 
     def step(self, depth, obj_state, sen_state):
-        if self._graph is not None and self._graph_inputs[0] is depth:
-            self.replay()
+        if self._graph is not None and all(a is b for a, b in zip(self._graph_inputs,
+                                                                   (depth, obj_state, sen_state))):
+            self.replay()  # the graph reads the captured tensors: replay only for those very inputs
         else:
             self.launch(depth, obj_state, sen_state)
         return self.rgb_u8 if self.rgb_u8 is not None else self.rgb_f32, self.f_n, self.f_t, self.wrench
+
+    def outputs(self):
+        """(name, device tensor) of every output of a step, in a fixed order."""
+        outs = [("rgb", self.rgb_u8), ("rgb_f32", self.rgb_f32)]
+        outs += [(f"rgb_l{lvl}", self.rgb_levels[lvl]) for lvl in range(1, self.levels)]
+        outs += [("f_n", self.f_n), ("f_t", self.f_t), ("wrench", self.wrench)]
+        return [(k, v) for k, v in outs if v is not None]
+
+    def frame_digests(self):
+        return frame_digests(self.outputs())
 
     def host_buffers(self, pinned=True):
         """Pinned host mirrors of the step's inputs and outputs."""
@@ -344,6 +361,33 @@ def shard_range(n_envs: int, rank: int, world: int):
     base, rem = divmod(n_envs, world)
     lo = rank * base + min(rank, rem)
     return lo, lo + base + (1 if rank < rem else 0)
+
+
+def frame_digests(outputs):
+    """Per-frame 64-bit digests (tacsl_frame_digest) of a step's outputs.
+
+    outputs: list of (name, tensor) with tensors of shape (E, S, ...) on the
+    device (None entries are skipped).  Returns (names, (E*S, k) int64 CUDA
+    tensor): column j is the digest of frame f of output j -- position
+    dependent, and the same for a frame whichever rank or batch computed it,
+    so the concatenation over ranks in env order is the N=1 list."""
+    from . import _lib
+
+    t = _device.torch()
+    names, cols = [], []
+    for name, x in outputs:
+        if x is None:
+            continue
+        n = int(x.shape[0]) * int(x.shape[1])
+        if not x.is_contiguous():
+            x = x.contiguous()
+        fb = x.numel() // max(n, 1) * x.element_size()
+        out = t.empty(n, dtype=t.int64, device=x.device)
+        _lib.check(_lib.load().tacsl_frame_digest(x.data_ptr(), n, fb, out.data_ptr(),
+                                                  _device.stream_handle(x.device)))
+        names.append(name)
+        cols.append(out)
+    return names, t.stack(cols, dim=1) if cols else None
 
 
 def frame_checksum(rgb_u8, f_n, f_t) -> np.ndarray:

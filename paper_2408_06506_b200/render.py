@@ -196,7 +196,7 @@ def depth_to_rgb(depth, lut, out_dtype=None):
         raise LutResolutionMismatch(f"LUT calibrated at {tuple(lut.image_size)}, image is {(W, H)}")
     on_device = _device.is_cuda_tensor(values)
     dev = _device.resolve_device(values.device if on_device else None)
-    v = _device.to_device(values, t.float32, dev)
+    v = _device.as_f32(values, dev)  # float64 depth is narrowed on the device
     want_u8 = out_dtype in (np.uint8, t.uint8, "uint8")
     shape = tuple(v.shape) + (3,)
     if want_u8:
@@ -207,13 +207,17 @@ def depth_to_rgb(depth, lut, out_dtype=None):
         depth_to_rgb_device(v, lut, out_f32=out)
     if on_device:
         return out
-    host = out.cpu().numpy()
-    return host if want_u8 else host.astype(np.float64)
+    if want_u8:
+        return out.cpu().numpy()
+    return _device.widen_f64(out).cpu().numpy()  # the reference's float64, widened on the device
 
 
 def to_uint8(img):
     """Drop-in for gelsim.render.to_uint8 (imageio.py:8-11): clip(rint(255 x)).
-    uint8 input is returned as is; float input is quantised on the GPU."""
+    uint8 input is returned as is; float input is quantised on the GPU --
+    float32 in float32 (the exact product of an fp32 value, = numpy's float64
+    product), everything else in float64 as the reference does, so the
+    result is bit-exact for either."""
     t = _device.torch()
     if isinstance(img, np.ndarray) and img.dtype == np.uint8:
         return img
@@ -221,7 +225,10 @@ def to_uint8(img):
         return img
     on_device = _device.is_cuda_tensor(img)
     dev = _device.resolve_device(img.device if on_device else None)
-    x = _device.to_device(img, t.float32, dev)
+    src_dtype = img.dtype if on_device else np.asarray(img).dtype
+    f32 = src_dtype in (t.float32, np.float32, t.float16, np.float16)
+    x = _device.to_device(img, t.float32 if f32 else t.float64, dev)
     out = t.empty(x.shape, dtype=t.uint8, device=dev)
-    _lib.check(_lib.load().tacsl_to_uint8(x.data_ptr(), x.numel(), out.data_ptr(), _device.stream_handle(dev)))
+    fn = _lib.load().tacsl_to_uint8 if f32 else _lib.load().tacsl_to_uint8_f64
+    _lib.check(fn(x.data_ptr(), x.numel(), out.data_ptr(), _device.stream_handle(dev)))
     return out if on_device else out.cpu().numpy()

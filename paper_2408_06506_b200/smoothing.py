@@ -72,6 +72,43 @@ def level_lut(lut, level: int) -> PolyLut:
     return PolyLut(degree=lut.degree, coeffs=coeffs, image_size=(W, H))
 
 
+def fused_pyramid_supported(H, W, levels, sigma=0.0, truncate=4.0) -> bool:
+    """Whether K7 (tacsl_rgb_pyramid, one pass) serves this shape."""
+    radius = (len(gaussian_taps(sigma, truncate)) - 1) // 2 if sigma > 0 else 0
+    return bool(_lib.load().tacsl_rgb_pyramid_supported(int(H), int(W), radius, int(levels)))
+
+
+def rgb_pyramid_fused_device(depth, lut, levels=3, sigma=0.0, truncate=4.0, outs=None, luts=None):
+    """K7: smoothing + every pyramid level's uint8 RGB in ONE kernel pass
+    (bit-identical to rgb_pyramid_device's level-by-level chain).  depth
+    (..., H, W) float32 CUDA; returns the list of (..., H >> l, W >> l, 3)
+    uint8 tensors (``outs`` to reuse buffers; ``luts`` the level DeviceLuts)."""
+    import ctypes
+
+    from .render import device_lut
+
+    t = _device.torch()
+    d = depth
+    if not (_device.is_cuda_tensor(d) and d.dtype == t.float32 and d.is_contiguous()):
+        raise TypeError("rgb_pyramid_fused_device wants a contiguous float32 CUDA tensor")
+    H, W = int(d.shape[-2]), int(d.shape[-1])
+    n = int(np.prod(d.shape[:-2], dtype=np.int64)) if d.ndim > 2 else 1
+    taps = gaussian_taps(sigma, truncate) if sigma > 0 else np.array([1.0])
+    radius = (len(taps) - 1) // 2
+    taps32 = np.ascontiguousarray(taps.astype(np.float32))
+    if luts is None:
+        luts = [device_lut(level_lut(lut, lvl)) for lvl in range(levels)]
+    if outs is None:
+        outs = [t.empty(tuple(d.shape[:-2]) + (H >> lvl, W >> lvl, 3), dtype=t.uint8, device=d.device)
+                for lvl in range(levels)]
+    handles = (ctypes.c_void_p * levels)(*[lu.handle.value for lu in luts])
+    ptrs = (ctypes.c_void_p * levels)(*[o.data_ptr() for o in outs])
+    _lib.check(_lib.load().tacsl_rgb_pyramid(ctypes.addressof(handles), levels, d.data_ptr(), n, H, W,
+                                             taps32.ctypes.data, radius, ctypes.addressof(ptrs),
+                                             _device.stream_handle(d.device)))
+    return outs
+
+
 def rgb_pyramid_device(depth, lut, levels=3, sigma=0.0, truncate=4.0):
     """Multi-scale tactile RGB: optional Gaussian smoothing of the full-res
     depth, then `levels` uint8 RGB images, level l at 2^-l resolution.

@@ -20,7 +20,8 @@ def run_bench(*args):
 
 
 def test_bench_json_contract():
-    d = run_bench("--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "2", "--settle", "0")
+    d = run_bench("--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "2", "--settle", "0",
+                  "--sustain-s", "0.2")
     for k, typ in (("metric", str), ("value", float), ("unit", str), ("n_gpus", int), ("steps", int),
                    ("warmup", int), ("ms_per_step", float), ("higher_is_better", bool), ("scaling", str),
                    ("dtype", str), ("data", str), ("config", dict), ("e2e", dict), ("roofline", dict),
@@ -36,6 +37,9 @@ def test_bench_json_contract():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
+    assert d["parity"]["ok"] and d["parity"]["rgb_max_lsb"] <= 1 and d["parity"]["mask_mismatches"] == 0
+    assert len(d["validation"]["sha256"]) == 64 and d["validation"]["frames"] == 8192
+    assert d["value_sustained"] > 0 and d["sustained"]["seconds"] >= 0.15
 
 
 def test_bench_configs_run():
@@ -43,3 +47,38 @@ def test_bench_configs_run():
         d = run_bench("--config", cfg, "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
                       "--settle", "0")
         assert d["value"] > 0 and d["e2e"] is None
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_bench_two_ranks_match_one_rank():
+    """bench.py under torchrun with 2 ranks (gloo for the collectives, both
+    ranks on the one GPU of this box -- a functional check of the sharding and
+    of the validation gather, not a measurement): the gathered parity block is
+    green and the whole-job digest equals the N=1 run's."""
+    import os
+    common = ["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--settle", "0",
+              "--sustain-s", "0", "--envs", "512"]
+    one = run_bench(*common)
+    env = dict(os.environ, TACSL_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+                          str(ROOT / "bench.py"), "--gpus", "2", *common],
+                         capture_output=True, text=True, cwd=ROOT, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [line for line in out.stdout.splitlines() if line.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    two = json.loads(lines[0])
+    assert two["n_gpus"] == 2 and one["n_gpus"] == 1
+    assert one["parity"]["ok"] and two["parity"]["ok"], (one["parity"], two["parity"])
+    assert two["validation"]["sha256"] == one["validation"]["sha256"]
+    assert two["validation"]["frames"] == one["validation"]["frames"] == 1024
+    for k in ("rgb_max_lsb", "rgb_frac_off", "ff_max_rel", "mask_mismatches", "frames_checked"):
+        assert two["parity"][k] == one["parity"][k], k

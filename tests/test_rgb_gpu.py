@@ -141,3 +141,56 @@ def test_rgb_pipeline_shapes(monkeypatch, groups, stages):
 def test_to_uint8_is_bit_exact():
     x = np.concatenate([np.linspace(-0.1, 1.1, 100001), (np.arange(256) + 0.5) / 255.0]).astype(np.float32)
     np.testing.assert_array_equal(render.to_uint8(x), O.to_uint8(x.astype(np.float64)))
+
+
+def test_to_uint8_f64_is_bit_exact_at_rounding_boundaries():
+    # values whose 255*x sits on, or one float64 ulp either side of, k + 1/2:
+    # the f32-narrowing path of round 1 rounded some of these the other way
+    k = np.arange(-2, 257, dtype=np.float64)
+    mid = (k + 0.5) / 255.0
+    x = np.concatenate([mid, np.nextafter(mid, np.inf), np.nextafter(mid, -np.inf),
+                        np.nextafter(np.nextafter(mid, np.inf), np.inf),
+                        k / 255.0, np.linspace(-0.2, 1.2, 200003),
+                        np.array([0.0, -0.0, 1.0, np.inf, -np.inf, 1e300, -1e300])])
+    ref = np.clip(np.rint(x * 255), 0, 255).astype(np.uint8)  # imageio.py:8-11 verbatim
+    got = render.to_uint8(x)
+    np.testing.assert_array_equal(got, ref)
+    # and the f32-narrowed route really differs somewhere here (the test has teeth)
+    with np.errstate(over="ignore"):
+        x32 = x.astype(np.float32)
+    assert (render.to_uint8(x32) != ref).any()
+    # device float64 tensors take the same path
+    assert torch.equal(render.to_uint8(torch.from_numpy(x).cuda()).cpu(), torch.from_numpy(ref))
+
+
+def test_depth_to_rgb_float64_input_narrowed_on_device():
+    size = (320, 240)
+    _, cam, bg, lut, _ = synthetic.sensor_setup(size)
+    d64 = synthetic.depth_batch(cam, bg, 3, config_id=12).astype(np.float64)
+    d64 += np.random.default_rng(3).uniform(-1e-9, 1e-9, d64.shape)  # not f32-representable
+    a = depth_to_rgb(d64, lut, out_dtype=np.uint8)
+    b = depth_to_rgb(d64.astype(np.float32), lut, out_dtype=np.uint8)
+    np.testing.assert_array_equal(a, b)  # device narrowing == numpy astype(float32)
+    f = depth_to_rgb(render.DepthImage(values=d64, background=bg), lut)
+    assert f.dtype == np.float64 and f.shape == d64.shape + (3,)
+    ref = O.depth_to_rgb(d64, lut.coeffs, 2)
+    # the kernels shade in fp32: sub-ulp depth noise moves values by ~1e-5
+    np.testing.assert_allclose(f, ref, atol=3e-5)
+    check_u8(O.to_uint8(f), O.to_uint8(ref), max_frac=1e-3)
+    t64 = torch.from_numpy(d64).cuda()
+    assert torch.equal(depth_to_rgb(t64, lut, out_dtype=np.uint8).cpu(), torch.from_numpy(a))
+
+
+def test_dtype_conversions_round_like_numpy():
+    from paper_2408_06506_b200 import _device
+    rng = np.random.default_rng(5)
+    for n in (0, 1, 3, 4, 5, 1023, 100001):
+        x = rng.standard_normal(n) * 10.0 ** rng.integers(-30, 30, n)
+        g = _device.as_f32(x, torch.device("cuda", 0))
+        np.testing.assert_array_equal(g.cpu().numpy(), x.astype(np.float32))
+        w = _device.widen_f64(g)
+        np.testing.assert_array_equal(w.cpu().numpy(), x.astype(np.float32).astype(np.float64))
+    # unaligned views take the scalar path
+    x = rng.standard_normal(1001)
+    t = torch.from_numpy(x).cuda()[1:]
+    np.testing.assert_array_equal(_device.as_f32(t, t.device).cpu().numpy(), x[1:].astype(np.float32))

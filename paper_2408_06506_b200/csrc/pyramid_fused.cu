@@ -52,7 +52,6 @@ namespace {
 
 constexpr int kHalf = 4;         // input rows per TMA stage (half a tick)
 constexpr int kPMaxCons = 256;   // consumer threads per CTA: W <= 1024
-constexpr int kPMaxStages = 6;
 
 struct PyrArgs {
   float w[9];            // Gaussian taps, 2R+1
@@ -60,42 +59,36 @@ struct PyrArgs {
   float pw[5];           // pyramid taps [1, 4, 6, 4, 1] / 16
   LutParams L[3];        // level LUTs (level_lut: c_ij 2^-l(i+j)), pre-scaled like every K1 LUT
   uint8_t* out[3];       // (n, H_l, W_l, 3) uint8
-  int stages;
   int ticks;
 };
 
 template <int R>
-struct Ring {
-  static constexpr int S0 = 14 - R;  // 8 new rows + 2 read back + the R-row lag of the filter
-  static constexpr int S1 = 6;
-  static constexpr int S2 = 4;
+struct Ring {  // line-ring depths (rows), powers of two: slot = row & (S - 1)
+  static constexpr int S0 = 16;  // >= 8 new rows + 2 read back + the R-row lag of the filter
+  static constexpr int S1 = 8;   // >= 4 new + 2 read back
+  static constexpr int S2 = 4;   // >= 2 new + 2 read back
 };
+constexpr int kPad = 4;  // floats of edge padding on both sides of every ring row ('nearest' borders)
 
 __device__ __forceinline__ void pyr_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-// one level-0-style quad of a row: the thread's 4 columns, the two columns
-// to its left and the one to its right (clamped at the image borders)
-struct Quad {
-  float4 c;
-  float2 l;
-  float r;
-};
-
-// uint8 RGB of pixels (2 pairs) with K1's arithmetic: doubled gradients, the
-// level LUT's packed Horner, saturating last step, biased rounding, PRMT.
+// uint8 RGB of a column quad (two pixel pairs) with K1's arithmetic:
+// doubled gradients, the level LUT's packed Horner, saturating last step,
+// biased rounding, PRMT packing into three words.
 template <int DEG>
-__device__ __forceinline__ void shade_quad(const LutParams& L, const float4 up, const Quad& c, const float4 dn,
-                                           bool edge_row, float m0, float m3, uint32_t* __restrict__ dst) {
+__device__ __forceinline__ void shade_quad(const LutParams& L, const float4 up, const float4 c, float left,
+                                           float right, const float4 dn, bool edge_row, float m0, float m3,
+                                           uint32_t& w0, uint32_t& w1, uint32_t& w2) {
   float2 hy01 = __fadd2_rn(make_float2(dn.x, dn.y), make_float2(-up.x, -up.y));
   float2 hy23 = __fadd2_rn(make_float2(dn.z, dn.w), make_float2(-up.z, -up.w));
   if (edge_row) {
     hy01 = __fadd2_rn(hy01, hy01);
     hy23 = __fadd2_rn(hy23, hy23);
   }
-  const float2 hx01 = make_float2((c.c.y - c.l.y) * m0, c.c.z - c.c.x);
-  const float2 hx23 = make_float2(c.c.w - c.c.y, (c.r - c.c.z) * m3);
+  const float2 hx01 = make_float2((c.y - left) * m0, c.z - c.x);
+  const float2 hx23 = make_float2(c.w - c.y, (right - c.z) * m3);
   const float2 r01 = poly2_sat<DEG>(L.c[0], hx01, hy01);
   const float2 g01 = poly2_sat<DEG>(L.c[1], hx01, hy01);
   const float2 b01 = poly2_sat<DEG>(L.c[2], hx01, hy01);
@@ -108,19 +101,19 @@ __device__ __forceinline__ void shade_quad(const LutParams& L, const float4 up, 
   const float2 qd = q8x2(make_float2(r23.x, g23.x));
   const float2 qe = q8x2(make_float2(b23.x, r23.y));
   const float2 qf = q8x2(make_float2(g23.y, b23.y));
-  dst[0] = __byte_perm(__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040),
-                       __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040), 0x5410);
-  dst[1] = __byte_perm(__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040),
-                       __byte_perm(__float_as_uint(qd.x), __float_as_uint(qd.y), 0x0040), 0x5410);
-  dst[2] = __byte_perm(__byte_perm(__float_as_uint(qe.x), __float_as_uint(qe.y), 0x0040),
-                       __byte_perm(__float_as_uint(qf.x), __float_as_uint(qf.y), 0x0040), 0x5410);
+  w0 = __byte_perm(__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040),
+                   __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040), 0x5410);
+  w1 = __byte_perm(__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040),
+                   __byte_perm(__float_as_uint(qd.x), __float_as_uint(qd.y), 0x0040), 0x5410);
+  w2 = __byte_perm(__byte_perm(__float_as_uint(qe.x), __float_as_uint(qe.y), 0x0040),
+                   __byte_perm(__float_as_uint(qf.x), __float_as_uint(qf.y), 0x0040), 0x5410);
 }
 
-// a pixel pair (level 1): 6 bytes as three 16-bit stores
+// a pixel pair (level 1): 6 bytes as three 16-bit halves
 template <int DEG>
 __device__ __forceinline__ void shade_pair(const LutParams& L, float2 up, float2 c, float left, float right,
-                                           float2 dn, bool edge_row, float m0, float m1,
-                                           uint16_t* __restrict__ dst) {
+                                           float2 dn, bool edge_row, float m0, float m1, uint32_t& h0,
+                                           uint32_t& h1, uint32_t& h2) {
   float2 hy = __fadd2_rn(dn, make_float2(-up.x, -up.y));
   if (edge_row) hy = __fadd2_rn(hy, hy);
   const float2 hx = make_float2((c.y - left) * m0, (right - c.x) * m1);
@@ -130,9 +123,9 @@ __device__ __forceinline__ void shade_pair(const LutParams& L, float2 up, float2
   const float2 qa = q8x2(make_float2(r.x, g.x));
   const float2 qb = q8x2(make_float2(b.x, r.y));
   const float2 qc = q8x2(make_float2(g.y, b.y));
-  dst[0] = (uint16_t)__byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040);
-  dst[1] = (uint16_t)__byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040);
-  dst[2] = (uint16_t)__byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040);
+  h0 = __byte_perm(__float_as_uint(qa.x), __float_as_uint(qa.y), 0x0040);
+  h1 = __byte_perm(__float_as_uint(qb.x), __float_as_uint(qb.y), 0x0040);
+  h2 = __byte_perm(__float_as_uint(qc.x), __float_as_uint(qc.y), 0x0040);
 }
 
 // horizontal pyramid tap sum at one output column from the 5 input columns
@@ -144,8 +137,16 @@ __device__ __forceinline__ float pyr_h(const float* pw, float a, float b, float 
   return ev + od;
 }
 
+// Shared-memory layout (floats after a 128-byte barrier block):
+//   input ring : 2 x 4 rows x (W + 8)        (TMA writes columns 4 .. W+3)
+//   S0 ring    : 16 x (W + 8)    smoothed level-0 rows
+//   S1 ring    : 8 x (W/2 + 8)   level-1 depth rows
+//   S2 ring    : 4 x (W/4 + 8)   level-2 depth rows
+// Every row carries 4 padding floats on each side holding its edge value
+// ('nearest' borders), written by the edge thread that owns the edge
+// column -- so no thread ever selects a clamped neighbour in the row loops.
 template <int R, int LEVELS, int DEG>
-__global__ void __launch_bounds__(kPMaxCons + 32, 1)
+__global__ void __maxnreg__(128)
     pyramid_fused_kernel(const float* __restrict__ depth, int64_t n, int H, int W, const PyrArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   using RG = Ring<R>;
@@ -154,64 +155,55 @@ __global__ void __launch_bounds__(kPMaxCons + 32, 1)
   const int cons_warps = (NQ + 31) >> 5;
   const int n_cons = cons_warps * 32;
   const int H1 = H >> 1, H2 = H >> 2, W1 = W >> 1, W2 = W >> 2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kPMaxStages;
+  const int WP = W + 2 * kPad, W1P = W1 + 2 * kPad, W2P = W2 + 2 * kPad;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // full[h]: half h of the tick's input rows landed
   float* in_buf = reinterpret_cast<float*>(smem + 128);
-  const size_t stage_f = (size_t)kHalf * W;
-  float* s0 = in_buf + (size_t)A.stages * stage_f;
-  float* s1 = s0 + (size_t)RG::S0 * W;
-  float* s2 = s1 + (size_t)RG::S1 * W1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int stage_f = kHalf * WP;
+  float* s0 = in_buf + 2 * stage_f;
+  float* s1 = s0 + RG::S0 * WP;
+  float* s2 = s1 + RG::S1 * W1P;
   const int K = A.ticks;
   const int kG = (H + 7) >> 3;  // last tick with input rows (8k - 4 <= H + 3)
-  const int stages = A.stages;
+
+  // Input rows of tick k, image img, into the two half stages: issued by
+  // thread 0 once every consumer has finished the previous tick's G phase
+  // (the named barrier that follows it), so the stages need no "empty"
+  // handshake and the CTA has no producer warp (3 CTAs per SM fit the
+  // register file and shared memory).
+  auto issue_tick = [&](int64_t img, int k) {
+    fence_proxy_async_smem();  // the stage's generic-proxy reads happen before the async overwrite
+    const float* src = depth + (size_t)img * H * W;
+    const uint32_t row_bytes = (uint32_t)W * 4u;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j0 = 8 * k - 4 + kHalf * h;
+      float* dst = in_buf + h * stage_f + kPad;
+      mbar_arrive_expect_tx(&full[h], kHalf * row_bytes);
+      // rows outside the image arrive as the clamped edge row ('nearest')
+#pragma unroll
+      for (int i = 0; i < kHalf; ++i) {
+        const int r = min(max(j0 + i, 0), H - 1);
+        bulk_g2s(dst + i * WP, src + (size_t)r * W, row_bytes, &full[h]);
+      }
+    }
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], cons_warps);
-    }
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
     fence_mbar_init();
     fence_proxy_async_smem();
+    if (blockIdx.x < n) issue_tick(blockIdx.x, 0);
   }
   __syncthreads();
 
-  if (warp == cons_warps) {
-    // ---------------------------------------------------------- loader ---
-    if (lane == 0) {
-      int q = 0;
-      const uint32_t row_bytes = (uint32_t)W * 4u;
-      for (int64_t img = blockIdx.x; img < n; img += gridDim.x) {
-        const float* src = depth + (size_t)img * H * W;
-        for (int k = 0; k <= kG; ++k) {
-          for (int h = 0; h < 2; ++h, ++q) {
-            const int s = q % stages;
-            if (q >= stages) mbar_wait_parity_sleep(&empty[s], (uint32_t)(q / stages - 1) & 1u);
-            const int j0 = 8 * k - 4 + kHalf * h;
-            float* dst = in_buf + (size_t)s * stage_f;
-            mbar_arrive_expect_tx(&full[s], kHalf * row_bytes);
-            if (j0 >= 0 && j0 + kHalf <= H) {
-              bulk_g2s(dst, src + (size_t)j0 * W, kHalf * row_bytes, &full[s]);
-            } else {  // rows outside the image: the clamped edge row ('nearest')
-              for (int i = 0; i < kHalf; ++i) {
-                const int r = min(max(j0 + i, 0), H - 1);
-                bulk_g2s(dst + (size_t)i * W, src + (size_t)r * W, row_bytes, &full[s]);
-              }
-            }
-          }
-        }
-      }
-    }
-    return;
-  }
-
   // ------------------------------------------------------------ consumers ---
-  const int t = threadIdx.x;
-  const bool act = t < NQ;
+  const bool act = (int)threadIdx.x < NQ;
+  const int t = min((int)threadIdx.x, NQ - 1);  // padding lanes shadow the last quad, store nothing
   const int x0 = 4 * t;
-  const bool atL = t == 0, atR = t == NQ - 1;
-  const float m0 = atL ? 2.f : 1.f;  // np.gradient's one-sided borders are not halved
-  const float m3 = atR ? 2.f : 1.f;
+  const bool atL = act && t == 0, atR = act && t == NQ - 1;
+  const float m0 = t == 0 ? 2.f : 1.f;  // np.gradient's one-sided borders are not halved
+  const float m3 = t == NQ - 1 ? 2.f : 1.f;
   float2 acc[8][2];  // vertical Gaussian accumulators, slot = output row & 7
   float2 acc1[2];    // level-1 vertical accumulators (column pair), slot = row & 1
   float acc2[2];     // level-2 vertical accumulators, slot = row & 1
@@ -219,45 +211,47 @@ __global__ void __launch_bounds__(kPMaxCons + 32, 1)
   for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = f2(0.f, 0.f);
   acc1[0] = acc1[1] = f2(0.f, 0.f);
   acc2[0] = acc2[1] = 0.f;
-  int q = 0;
+  uint32_t ph = 0;  // phase of both half stages (each completes once per G tick)
+  const int W3 = 3 * W, W13 = 3 * W1, W23 = 3 * W2;
 
   for (int64_t img = blockIdx.x; img < n; img += gridDim.x) {
-    uint8_t* out0 = A.out[0] + (size_t)img * H * W * 3;
-    uint8_t* out1 = LEVELS >= 2 ? A.out[1] + (size_t)img * H1 * W1 * 3 : nullptr;
-    uint8_t* out2 = LEVELS >= 3 ? A.out[2] + (size_t)img * H2 * W2 * 3 : nullptr;
+    uint8_t* out0 = A.out[0] + (size_t)img * H * W3 + 3 * x0;
+    uint8_t* out1 = LEVELS >= 2 ? A.out[1] + (size_t)img * H1 * W13 + 6 * t : nullptr;
+    uint8_t* out2 = LEVELS >= 3 ? A.out[2] + (size_t)img * H2 * W23 + 3 * t : nullptr;
     for (int k = 0; k < K; ++k) {
       // ------------------------------------------------------------ G ---
       if (k <= kG) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int s = q % stages;
-          mbar_wait_parity(&full[s], (uint32_t)(q / stages) & 1u);
-          const float* st = in_buf + (size_t)s * stage_f;
+          mbar_wait_parity(&full[h], ph);
+          float* st = in_buf + h * stage_f;
+          if (atL) {  // left padding = column 0 of each row
+#pragma unroll
+            for (int i = 0; i < kHalf; ++i) {
+              const float v = st[i * WP + kPad];
+              *reinterpret_cast<float4*>(st + i * WP) = make_float4(v, v, v, v);
+            }
+          }
+          if (atR) {  // right padding = column W-1
+#pragma unroll
+            for (int i = 0; i < kHalf; ++i) {
+              const float v = st[i * WP + kPad + W - 1];
+              *reinterpret_cast<float4*>(st + i * WP + kPad + W) = make_float4(v, v, v, v);
+            }
+          }
 #pragma unroll
           for (int i = 0; i < kHalf; ++i) {
             const int ii = kHalf * h + i;  // h-row j = 8k - 4 + ii
-            const int j = 8 * k - 4 + ii;
-            const float* row = st + (size_t)i * W;
-            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-            bool done = false;
+            const int y = 8 * k - 4 + ii - R;  // the smoothed row this h-row completes
+            const float* row = st + i * WP + kPad + x0;
+            float4 o;
             if constexpr (R == 0) {
-              if (act) o = *reinterpret_cast<const float4*>(row + x0);
-              done = true;
+              o = *reinterpret_cast<const float4*>(row);
             } else {
-              float v[12];
-              if (act) {
-                const float4 b = *reinterpret_cast<const float4*>(row + x0);
-                const float4 a = atL ? make_float4(b.x, b.x, b.x, b.x)
-                                     : *reinterpret_cast<const float4*>(row + x0 - 4);
-                const float4 c = atR ? make_float4(b.w, b.w, b.w, b.w)
-                                     : *reinterpret_cast<const float4*>(row + x0 + 4);
-                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-                v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-                v[8] = c.x; v[9] = c.y; v[10] = c.z; v[11] = c.w;
-              } else {
-#pragma unroll
-                for (int e = 0; e < 12; ++e) v[e] = 0.f;
-              }
+              const float4 va = *reinterpret_cast<const float4*>(row - 4);
+              const float4 vb = *reinterpret_cast<const float4*>(row);
+              const float4 vc = *reinterpret_cast<const float4*>(row + 4);
+              const float v[12] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w, vc.x, vc.y, vc.z, vc.w};
               // horizontal: sep_bulk_kernel's FFMA2 over (even, odd) column
               // pairs of v (v[0] on an even column), partial sums added last
               float hq[4];
@@ -284,71 +278,78 @@ __global__ void __launch_bounds__(kPMaxCons + 32, 1)
                   const float2 o01 = __ffma2_rn(h01, w, acc[slot][0]);
                   const float2 o23 = __ffma2_rn(h23, w, acc[slot][1]);
                   o = make_float4(o01.x, o01.y, o23.x, o23.y);
-                  done = true;
-                } else if (tt == 0) {
-                  acc[slot][0] = __ffma2_rn(h01, w, f2(0.f, 0.f));
-                  acc[slot][1] = __ffma2_rn(h23, w, f2(0.f, 0.f));
                 } else {
-                  acc[slot][0] = __ffma2_rn(h01, w, acc[slot][0]);
-                  acc[slot][1] = __ffma2_rn(h23, w, acc[slot][1]);
+                  acc[slot][0] = __ffma2_rn(h01, w, tt == 0 ? f2(0.f, 0.f) : acc[slot][0]);
+                  acc[slot][1] = __ffma2_rn(h23, w, tt == 0 ? f2(0.f, 0.f) : acc[slot][1]);
                 }
               }
             }
-            const int y = j - R;  // the smoothed row this h-row completes
-            if (done && act && y >= 0 && y < H)
-              *reinterpret_cast<float4*>(s0 + (size_t)(y % RG::S0) * W + x0) = o;
+            if (y >= 0 && y < H) {
+              float* dst = s0 + (y & (RG::S0 - 1)) * WP + kPad;
+              if (act) *reinterpret_cast<float4*>(dst + x0) = o;
+              if (atL) *reinterpret_cast<float2*>(dst - 2) = f2(o.x, o.x);
+              if (atR) dst[W] = o.w;
+            }
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
-          ++q;
         }
+        ph ^= 1u;
       }
-      pyr_bar(n_cons);  // S0 rows of this tick are visible
+      pyr_bar(n_cons);  // S0 rows of this tick are visible; the input stages are free
+      if (threadIdx.x == 0) {
+        if (k < kG) issue_tick(img, k + 1);
+        else if (k == kG && img + gridDim.x < n) issue_tick(img + gridDim.x, 0);
+      }
 
       // ----------------------------------------------------------- L0 ---
       if (k >= 1) {
         const int sb = 8 * k - 10;
-        Quad win[3];  // rows s-2, s-1, s
+        float4 wq[3];  // quads of rows s-2, s-1, s
+        float wl = 0.f, wr = 0.f;  // left / right neighbour of row s-1
+        uint8_t* orow = out0 + (sb + 1) * W3;  // row s-1 at m = 2
 #pragma unroll
         for (int m = 0; m < 10; ++m) {
-          const int s = sb + m;
-          const int r = min(max(s, 0), H - 1);
-          const float* rp = s0 + (size_t)(r % RG::S0) * W;
-          Quad cur;
-          if (act) {
-            cur.c = *reinterpret_cast<const float4*>(rp + x0);
-            cur.l = atL ? f2(cur.c.x, cur.c.x) : *reinterpret_cast<const float2*>(rp + x0 - 2);
-            cur.r = atR ? cur.c.w : rp[x0 + 4];
-          } else {
-            cur.c = make_float4(0.f, 0.f, 0.f, 0.f);
-            cur.l = f2(0.f, 0.f);
-            cur.r = 0.f;
-          }
-          win[0] = win[1];
-          win[1] = win[2];
-          win[2] = cur;
+          const int sr = sb + m;
+          const int r = min(max(sr, 0), H - 1);
+          const float* rp = s0 + (r & (RG::S0 - 1)) * WP + kPad + x0;
+          const float4 c = *reinterpret_cast<const float4*>(rp);
+          const float2 l = *reinterpret_cast<const float2*>(rp - 2);
+          const float rr = rp[4];
+          wq[0] = wq[1];
+          wq[1] = wq[2];
+          wq[2] = c;
           if (m >= 2) {
-            const int y = s - 1;
-            if (act && y >= 0 && y < H)
-              shade_quad<DEG>(A.L[0], win[0].c, win[1], win[2].c, y == 0 || y == H - 1, m0, m3,
-                              reinterpret_cast<uint32_t*>(out0 + ((size_t)y * W + x0) * 3));
+            const int y = sr - 1;
+            uint32_t w0, w1, w2;
+            shade_quad<DEG>(A.L[0], wq[0], wq[1], wl, wr, wq[2], y == 0 || y == H - 1, m0, m3, w0, w1, w2);
+            if (act && y >= 0 && y < H) {
+              uint32_t* o = reinterpret_cast<uint32_t*>(orow);
+              o[0] = w0;
+              o[1] = w1;
+              o[2] = w2;
+            }
+            orow += W3;
           }
+          wl = l.y;
+          wr = rr;
           if constexpr (LEVELS >= 2) {
             if (m < 8) {
-              // virtual S0 row i = s (row clamp(i)) decimated at level-1
+              // virtual S0 row i = sr (row clamp(i)) decimated at level-1
               // columns 2t, 2t+1 (input columns 4t-2 .. 4t+4)
-              const float2 hp = f2(pyr_h(A.pw, cur.l.x, cur.l.y, cur.c.x, cur.c.y, cur.c.z),
-                                   pyr_h(A.pw, cur.c.x, cur.c.y, cur.c.z, cur.c.w, cur.r));
+              const float2 hp = f2(pyr_h(A.pw, l.x, l.y, c.x, c.y, c.z), pyr_h(A.pw, c.x, c.y, c.z, c.w, rr));
 #pragma unroll
               for (int tt = 4; tt >= 0; --tt) {
                 if (((m - tt) & 1) != 0) continue;
-                const int y1 = (s + 2 - tt) >> 1;  // s + 2 - tt is even
-                if (y1 < 0 || y1 >= H1) continue;
-                const int slot = ((m - tt + 8) >> 1) & 1;
+                const int slot = ((m - tt + 8) >> 1) & 1;  // (level-1 row) & 1
                 const float2 w = f2(A.pw[tt], A.pw[tt]);
                 if (tt == 4) {
                   const float2 o = __ffma2_rn(hp, w, acc1[slot]);
-                  if (act) *reinterpret_cast<float2*>(s1 + (size_t)(y1 % RG::S1) * W1 + 2 * t) = o;
+                  const int y1 = (sr + 2 - tt) >> 1;  // sr + 2 - tt is even
+                  if (y1 >= 0 && y1 < H1) {
+                    float* dst = s1 + (y1 & (RG::S1 - 1)) * W1P + kPad;
+                    if (act) *reinterpret_cast<float2*>(dst + 2 * t) = o;
+                    if (atL) *reinterpret_cast<float2*>(dst - 2) = f2(o.x, o.x);
+                    if (atR) dst[W1] = o.y;
+                  }
                 } else {
                   acc1[slot] = __ffma2_rn(hp, w, tt == 0 ? f2(0.f, 0.f) : acc1[slot]);
                 }
@@ -363,46 +364,55 @@ __global__ void __launch_bounds__(kPMaxCons + 32, 1)
       if constexpr (LEVELS >= 2) {
         if (k >= 1) {
           const int sb = 4 * k - 8;
-          float2 wc[3], wl[3];
-          float wr[3];
+          float2 wc[3];
+          float wl = 0.f, wr = 0.f;
+          uint8_t* orow = out1 + (sb + 1) * W13;
 #pragma unroll
           for (int m = 0; m < 6; ++m) {
-            const int s = sb + m;
-            const int r = min(max(s, 0), H1 - 1);
-            const float* rp = s1 + (size_t)(r % RG::S1) * W1;
-            float2 c = f2(0.f, 0.f), l = f2(0.f, 0.f);
-            float rr = 0.f;
-            if (act) {
-              c = *reinterpret_cast<const float2*>(rp + 2 * t);
-              l = atL ? f2(c.x, c.x) : *reinterpret_cast<const float2*>(rp + 2 * t - 2);
-              rr = atR ? c.y : rp[2 * t + 2];
-            }
-            wc[0] = wc[1]; wc[1] = wc[2]; wc[2] = c;
-            wl[0] = wl[1]; wl[1] = wl[2]; wl[2] = l;
-            wr[0] = wr[1]; wr[1] = wr[2]; wr[2] = rr;
+            const int sr = sb + m;
+            const int r = min(max(sr, 0), H1 - 1);
+            const float* rp = s1 + (r & (RG::S1 - 1)) * W1P + kPad + 2 * t;
+            const float2 c = *reinterpret_cast<const float2*>(rp);
+            const float2 l = *reinterpret_cast<const float2*>(rp - 2);
+            const float rr = rp[2];
+            wc[0] = wc[1];
+            wc[1] = wc[2];
+            wc[2] = c;
             if (m >= 2) {
-              const int y = s - 1;
-              if (act && y >= 0 && y < H1)
-                shade_pair<DEG>(A.L[1], wc[0], wc[1], wl[1].y, wr[1], wc[2], y == 0 || y == H1 - 1, m0, m3,
-                                reinterpret_cast<uint16_t*>(out1 + ((size_t)y * W1 + 2 * t) * 3));
+              const int y = sr - 1;
+              uint32_t h0, h1, h2;
+              shade_pair<DEG>(A.L[1], wc[0], wc[1], wl, wr, wc[2], y == 0 || y == H1 - 1, m0, m3, h0, h1, h2);
+              if (act && y >= 0 && y < H1) {
+                uint16_t* o = reinterpret_cast<uint16_t*>(orow);
+                o[0] = (uint16_t)h0;
+                o[1] = (uint16_t)h1;
+                o[2] = (uint16_t)h2;
+              }
+              orow += W13;
               if constexpr (LEVELS >= 3) {
-                // virtual level-1 row i = s decimated at level-2 column t
+                // virtual level-1 row i = sr decimated at level-2 column t
                 const float hv = pyr_h(A.pw, l.x, l.y, c.x, c.y, rr);
 #pragma unroll
                 for (int tt = 4; tt >= 0; --tt) {
                   if (((m - tt) & 1) != 0) continue;
-                  const int y2 = (s + 2 - tt) >> 1;
-                  if (y2 < 0 || y2 >= H2) continue;
-                  const int slot = ((m - tt + 2) >> 1) & 1;
+                  const int slot = ((m - tt + 2) >> 1) & 1;  // (level-2 row) & 1
                   if (tt == 4) {
                     const float o = __fmaf_rn(hv, A.pw[4], acc2[slot]);
-                    if (act) s2[(size_t)(y2 & (RG::S2 - 1)) * W2 + t] = o;
+                    const int y2 = (sr + 2 - tt) >> 1;
+                    if (y2 >= 0 && y2 < H2) {
+                      float* dst = s2 + (y2 & (RG::S2 - 1)) * W2P + kPad;
+                      if (act) dst[t] = o;
+                      if (atL) dst[-1] = o;
+                      if (atR) dst[W2] = o;
+                    }
                   } else {
                     acc2[slot] = __fmaf_rn(hv, A.pw[tt], tt == 0 ? 0.f : acc2[slot]);
                   }
                 }
               }
             }
+            wl = l.y;
+            wr = rr;
           }
         }
       }
@@ -411,36 +421,35 @@ __global__ void __launch_bounds__(kPMaxCons + 32, 1)
         // --------------------------------------------------------- L2 ---
         if (k >= 1) {
           const int sb = 2 * k - 6;
-          float wc[3], wl[3], wr[3];
+          float wc[3];
+          float wl = 0.f, wr = 0.f;
+          uint8_t* orow = out2 + (sb + 1) * W23;
+          const float mx = (t == 0 || t == NQ - 1) ? 2.f : 1.f;
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
-            const int s = sb + m;
-            const int r = min(max(s, 0), H2 - 1);
-            const float* rp = s2 + (size_t)(r & (RG::S2 - 1)) * W2;
-            float c = 0.f, l = 0.f, rr = 0.f;
-            if (act) {
-              c = rp[t];
-              l = atL ? c : rp[t - 1];
-              rr = atR ? c : rp[t + 1];
-            }
-            wc[0] = wc[1]; wc[1] = wc[2]; wc[2] = c;
-            wl[0] = wl[1]; wl[1] = wl[2]; wl[2] = l;
-            wr[0] = wr[1]; wr[1] = wr[2]; wr[2] = rr;
+            const int sr = sb + m;
+            const int r = min(max(sr, 0), H2 - 1);
+            const float* rp = s2 + (r & (RG::S2 - 1)) * W2P + kPad + t;
+            const float c = rp[0];
+            wc[0] = wc[1];
+            wc[1] = wc[2];
+            wc[2] = c;
             if (m >= 2) {
-              const int y = s - 1;
-              const bool row_ok = y >= 0 && y < H2 && (m < 4 || y == H2 - 1);
-              if (act && row_ok) {
-                float hy = wc[2] - wc[0];
-                if (y == 0 || y == H2 - 1) hy = hy + hy;
-                const float hx = (wr[1] - wl[1]) * ((atL || atR) ? 2.f : 1.f);
-                float v0, v1, v2;
-                shade<DEG>(A.L[2], hx, hy, v0, v1, v2);
-                uint8_t* o = out2 + ((size_t)y * W2 + t) * 3;
-                o[0] = (uint8_t)(q8(v0) & 0xFFu);
-                o[1] = (uint8_t)(q8(v1) & 0xFFu);
-                o[2] = (uint8_t)(q8(v2) & 0xFFu);
+              const int y = sr - 1;
+              float hy = wc[2] - wc[0];
+              if (y == 0 || y == H2 - 1) hy = hy + hy;
+              const float hx = (wr - wl) * mx;
+              float v0, v1, v2;
+              shade<DEG>(A.L[2], hx, hy, v0, v1, v2);
+              if (act && y >= 0 && y < H2 && (m < 4 || y == H2 - 1)) {
+                orow[0] = (uint8_t)(q8(v0) & 0xFFu);
+                orow[1] = (uint8_t)(q8(v1) & 0xFFu);
+                orow[2] = (uint8_t)(q8(v2) & 0xFFu);
               }
+              orow += W23;
             }
+            wl = rp[-1];
+            wr = rp[1];
           }
         }
       }
@@ -456,20 +465,25 @@ int pyramid_ticks(int H, int levels) {
   return k;
 }
 
-size_t pyramid_smem(int R, int W, int stages) {
-  return 128 + (size_t)stages * kHalf * W * 4 + (size_t)(14 - R) * W * 4 + (size_t)6 * (W / 2) * 4 +
-         (size_t)4 * (W / 4) * 4;
+size_t pyramid_smem(int R, int W) {
+  (void)R;
+  const size_t WP = W + 2 * kPad, W1P = W / 2 + 2 * kPad, W2P = W / 4 + 2 * kPad;
+  return 128 + ((size_t)2 * kHalf * WP + 16 * WP + 8 * W1P + 4 * W2P) * 4;
 }
 
 template <int R, int LEVELS, int DEG>
 int launch_pyramid(const float* depth, int64_t n, int H, int W, PyrArgs& A, cudaStream_t stream) {
   auto kern = pyramid_fused_kernel<R, LEVELS, DEG>;
   if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), 227 * 1024)) return rc;
-  const char* e = std::getenv("TACSL_PYR_STAGES");
-  A.stages = std::min(std::max(e && *e ? std::atoi(e) : 3, 2), kPMaxStages);
+  static bool carve = false;  // all of the unified L1/shared array as shared memory: 3 CTAs per SM
+  if (!carve) {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   A.ticks = pyramid_ticks(H, LEVELS);
-  const size_t smem = pyramid_smem(R, W, A.stages);
-  const int threads = ((W / 4 + 31) / 32) * 32 + 32;
+  const size_t smem = pyramid_smem(R, W);
+  const int threads = ((W / 4 + 31) / 32) * 32;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb_pyramid: image too wide for shared memory");
@@ -508,7 +522,7 @@ extern "C" int tacsl_rgb_pyramid_supported(int height, int width, int radius, in
   if (levels < 1 || levels > 3 || radius < 0 || radius > 4) return 0;
   if (width < 8 || width % 4 != 0 || width / 4 > kPMaxCons) return 0;
   if (height < 4 || height % 4 != 0) return 0;
-  return pyramid_smem(radius, width, 2) <= 227 * 1024 ? 1 : 0;
+  return pyramid_smem(radius, width) <= 227 * 1024 ? 1 : 0;
 }
 
 extern "C" int tacsl_rgb_pyramid(const tacsl_lut_t* luts, int levels, const float* depth, int64_t n_images,

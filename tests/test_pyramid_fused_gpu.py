@@ -96,7 +96,7 @@ def _chain(d, lut, levels, sigma):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("hw", [(480, 640), (240, 320), (60, 80), (36, 44), (8, 8), (100, 1024), (484, 644)])
+@pytest.mark.parametrize("hw", [(480, 640), (240, 320), (60, 80), (36, 44), (8, 8), (100, 768), (484, 644)])
 @pytest.mark.parametrize("sigma", [0.0, 1.0])
 def test_fused_pyramid_bit_identical_to_chain(hw, sigma):
     import torch

@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     p.add_argument("--e2e-chunks", type=int, default=64, help="env chunks pipelined over H2D / compute / D2H")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample length")
+    p.add_argument("--dropin-frames", type=int, default=1024,
+                   help="sensor frames per call of the numpy drop-in e2e leg (0: skip)")
     p.add_argument("--sustain-s", type=float, default=1.5,
                    help="seconds of back-to-back steps for value_sustained (0: skip)")
     p.add_argument("--envs", type=int, default=None,
@@ -618,6 +620,64 @@ def main():
 
     e2e = None if args.no_e2e else measure_e2e()
 
+    # ---- end to end through the reference-signature numpy drop-ins (what a
+    # gelsim user gets after patch(): float64 numpy in, float64 numpy out)
+    def measure_dropin():
+        from paper_2408_06506_b200 import render, tactile
+        from paper_2408_06506_b200.render import DepthImage
+
+        S, H, W = c.S, c.H, c.W
+        envs = max(1, min(c.E, args.dropin_frames // S))
+        F = envs * S
+        g = np.arange(F) + c.lo * S
+        depth64 = c.pool[g % len(c.pool)].astype(np.float64).reshape(envs, S, H, W) if wl.rgb else None
+        objF = np.repeat(c.obj_all[c.lo:c.lo + envs], S, axis=0)
+        senF = c.sen_all[c.lo:c.lo + envs].reshape(F, 13)
+
+        def call():
+            out = {}
+            if wl.rgb:
+                out["rgb"] = render.depth_to_rgb(DepthImage(values=depth64, background=c.bg), c.lut)
+            if wl.ff:
+                out["ff"] = tactile.compute_force_field(
+                    c.pts, c.sdf, objF[:, 0:3], objF[:, 3:7], objF[:, 7:10], objF[:, 10:13],
+                    senF[:, 0:3], senF[:, 3:7], senF[:, 7:10], senF[:, 10:13], c.params)
+            return out
+
+        for _ in range(2):
+            call()
+        reps = max(2, args.e2e_steps // 2)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            out = call()
+        secs = max_over_ranks(time.perf_counter() - t0) / reps
+        h2d = (depth64.nbytes if wl.rgb else 0) + objF.nbytes + senF.nbytes
+        d2h = (out["rgb"].nbytes if wl.rgb else 0) + (out["ff"].f_n.nbytes * 2 if wl.ff else 0)
+        # the link's measured speed on this box (pinned, each direction alone)
+        a = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        dv = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        bw = {}
+        for name, (dst, src) in (("h2d", (dv, a)), ("d2h", (a, dv))):
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            for _ in range(4):
+                dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            bw[name] = 4 * a.numel() / (e0.elapsed_time(e1) / 1e3)
+        floor_s = max(h2d / bw["h2d"], d2h / bw["d2h"])  # copies in both directions overlapped
+        return {"value": F * world / secs, "unit": UNIT, "frames_per_call": F * world, "s_per_call": secs,
+                "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
+                "link_gbs": {k: v / 1e9 for k, v in bw.items()},
+                "pcie_floor_value": F * world / floor_s, "frac_of_pcie_floor": floor_s / secs,
+                "api": "render.depth_to_rgb(DepthImage float64 numpy) + tactile.compute_force_field(numpy poses) "
+                       "-> float64 numpy (the functions patch() binds into gelsim), wall clock per call pair"}
+
+    e2e_dropin = None if (args.no_e2e or args.dropin_frames <= 0) else measure_dropin()
+
     # ---- roofline of the dominant kernel (K1, or K2 when the step has no RGB) and of the whole step
     peak, peak_src = hbm_peak()
     bytes_ = arr.algorithmic_bytes()
@@ -651,6 +711,7 @@ def main():
         "data": "synthetic (analytic spherical-indenter depth maps, analytic peg SDF, random peg poses)",
         "config": workload_config(wl, world),
         "e2e": e2e,
+        "e2e_dropin": e2e_dropin,
         "value_sustained": sustained["value"] if sustained else None,
         "sustained": sustained,
         "roofline": {"bound": "hbm", "kernel": desc, "achieved": k_gbs,

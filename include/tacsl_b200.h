@@ -22,6 +22,7 @@
  *                           step's outputs for cross-rank validation
  *   tacsl_sdf_create        geometry/sdf.py:29-54 SdfGrid (device upload)
  *   tacsl_query_sdf         geometry/sdf.py:271-321 query_sdf
+ *   tacsl_relative_penetration_rate geometry/sdf.py:324-328 (INVALID_QUERY on out-of-grid queries)
  *   tacsl_penalty_forces    tactile/field.py:61-76 penalty_forces
  *   tacsl_force_field       tactile/field.py:79-129 compute_force_field
  *                           (+ net_wrench tactile/field.py:132-141 fused as a
@@ -180,6 +181,15 @@ TACSL_API int tacsl_to_uint8(const float* x, int64_t count, uint8_t* out, void* 
  * exactly as imageio.py:8-11 (product rounded to float64, ties to even;
  * NaN -> 0). */
 TACSL_API int tacsl_to_uint8_f64(const double* x, int64_t count, uint8_t* out, void* stream);
+
+/* geometry/sdf.py:324-328 relative_penetration_rate: out[i] = normal[i] .
+ * x_dot[i] (x_dot_broadcast: one x_dot (3,) for every query), summed left
+ * to right like np.einsum.  Returns INVALID_QUERY (InvalidQuery) when any
+ * valid[i] == 0, as the reference does; this needs the answer on the host,
+ * so the call synchronises `stream`.  scratch: one device int. */
+TACSL_API int tacsl_relative_penetration_rate(const double* normal, const uint8_t* valid, const double* x_dot,
+                                              int64_t n, int x_dot_broadcast, double* out, int* scratch,
+                                              void* stream);
 
 /* Element-wise dtype conversion on the device (round to nearest even, as
  * numpy's astype): the float64 arrays the reference's callers pass in are

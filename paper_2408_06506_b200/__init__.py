@@ -18,7 +18,7 @@ from .augment import AugmentConfig, augment
 from .binned import BinnedPolyLut, depth_to_rgb_binned
 from .depth import render_depth
 from .errors import DimensionMismatch, GelsimError, InvalidQuery, LutResolutionMismatch
-from .geometry import SdfGrid, SdfQuery, query_sdf, read_sdf_cache, write_sdf_cache
+from .geometry import SdfGrid, SdfQuery, query_sdf, read_sdf_cache, relative_penetration_rate, write_sdf_cache
 from .patching import patch, unpatch
 from .pipeline import SensorArray, shard_range
 from .render import DepthImage, PolyLut, depth_to_rgb, monomial_exponents, synthetic_lut, to_uint8
@@ -37,7 +37,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "DimensionMismatch", "GelsimError", "InvalidQuery", "LutResolutionMismatch",
-    "SdfGrid", "SdfQuery", "query_sdf", "read_sdf_cache", "write_sdf_cache",
+    "SdfGrid", "SdfQuery", "query_sdf", "read_sdf_cache", "relative_penetration_rate", "write_sdf_cache",
     "patch", "unpatch", "SensorArray", "shard_range",
     "envs", "formats", "AugmentConfig", "augment", "BinnedPolyLut", "depth_to_rgb_binned", "render_depth", "DepthImage", "PolyLut", "depth_to_rgb", "monomial_exponents", "synthetic_lut", "to_uint8",
     "TactileCamera", "TactileSensorSpec", "camera_for_sensor", "reference_depth",

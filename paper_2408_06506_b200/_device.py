@@ -94,3 +94,67 @@ def widen_f64(x):
     out = t.empty(x.shape, dtype=t.float64, device=x.device)
     _lib.check(_lib.load().tacsl_f32_to_f64(x.data_ptr(), x.numel(), out.data_ptr(), stream_handle(x.device)))
     return out
+
+
+# ---- host <-> device for the numpy drop-ins (pinned staging, pipelined)
+
+def pinned_empty(shape, dtype):
+    """A page-locked host tensor from torch's caching host allocator (blocks
+    are reused across calls once the tensors that held them are freed)."""
+    return torch().empty(tuple(shape), dtype=dtype, pin_memory=True)
+
+
+def to_pinned(arr, dtype):
+    """numpy -> page-locked host tensor of `dtype` (one host copy, which
+    torch spreads over the host's threads), for full-speed DMA uploads."""
+    t = torch()
+    src = t.from_numpy(np.ascontiguousarray(arr))
+    out = pinned_empty(src.shape, dtype)
+    out.copy_(src)
+    return out
+
+
+def download(x):
+    """CUDA tensor -> numpy array backed by page-locked memory (one DMA at
+    the link's speed into the array the caller receives; no extra host copy)."""
+    out = pinned_empty(x.shape, x.dtype)
+    out.copy_(x, non_blocking=True)
+    torch().cuda.current_stream(x.device).synchronize()
+    return out.numpy()
+
+
+def pipelined(host_in, host_out, fn, device, chunk):
+    """Run fn over the leading axis of pinned host tensors in chunks: chunk
+    i's upload, chunk i-1's kernels and chunk i-2's download overlap on three
+    streams (the two copy engines + the SMs).  fn(dev_ins, dev_outs) enqueues
+    its kernels on the current stream; device chunk buffers are double
+    buffered."""
+    t = torch()
+    n = host_in[0].shape[0]
+    main = t.cuda.current_stream(device)
+    up, down = t.cuda.Stream(device=device), t.cuda.Stream(device=device)
+    bufs = [([t.empty((chunk,) + tuple(h.shape[1:]), dtype=h.dtype, device=device) for h in host_in],
+             [t.empty((chunk,) + tuple(h.shape[1:]), dtype=h.dtype, device=device) for h in host_out])
+            for _ in range(2)]
+    free = [None, None]  # event: buffer set b may be overwritten (its download finished)
+    up.wait_stream(main)
+    for i, lo in enumerate(range(0, n, chunk)):
+        hi = min(lo + chunk, n)
+        b = i & 1
+        ins, outs = bufs[b]
+        with t.cuda.stream(up):
+            if free[b] is not None:
+                up.wait_event(free[b])
+            for d, h in zip(ins, host_in):
+                d[:hi - lo].copy_(h[lo:hi], non_blocking=True)
+        main.wait_stream(up)
+        fn([d[:hi - lo] for d in ins], [d[:hi - lo] for d in outs])
+        down.wait_stream(main)
+        with t.cuda.stream(down):
+            for d, h in zip(outs, host_out):
+                h[lo:hi].copy_(d[:hi - lo], non_blocking=True)
+            ev = t.cuda.Event()
+            ev.record(down)
+            free[b] = ev
+    main.wait_stream(down)
+    main.synchronize()

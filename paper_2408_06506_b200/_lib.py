@@ -44,6 +44,7 @@ SIGNATURES = {
     "tacsl_f64_to_f32": (c_int, [P, c_int64, P, c_void_p]),
     "tacsl_f32_to_f64": (c_int, [P, c_int64, P, c_void_p]),
     "tacsl_frame_digest": (c_int, [P, c_int64, c_int64, P, c_void_p]),
+    "tacsl_relative_penetration_rate": (c_int, [P, P, P, c_int64, c_int, P, P, c_void_p]),
     "tacsl_rgb_pyramid_supported": (c_int, [c_int, c_int, c_int, c_int]),
     "tacsl_rgb_pyramid": (c_int, [P, c_int, P, c_int64, c_int, c_int, P, c_int, P, c_void_p]),
     "tacsl_sdf_create": (c_int, [c_int, P, P, P, P, c_double, ctypes.POINTER(c_void_p)]),

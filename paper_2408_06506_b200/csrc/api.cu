@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(256) to_uint8_kernel(const float* __restrict__
 }  // namespace
 
 extern "C" int tacsl_to_uint8(const float* x, int64_t count, uint8_t* out, void* stream) {
+  StreamDevice stream_device_(stream);
   if (count < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "to_uint8: negative count");
   if (count == 0) return TACSL_OK;
   if (!x || !out) return set_error(TACSL_ERR_INVALID_ARGUMENT, "to_uint8: null pointer");

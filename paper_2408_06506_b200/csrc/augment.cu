@@ -363,6 +363,7 @@ using namespace tacsl;
 
 extern "C" int tacsl_augment_params(const tacsl_augment_cfg_t* cfg, const int64_t* episode_seeds,
                                     const int64_t* step_indices, int64_t n, double* params, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!cfg) return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: null config");
   if (n < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: negative count");
   if (n == 0) return TACSL_OK;
@@ -376,6 +377,7 @@ extern "C" int tacsl_augment_params(const tacsl_augment_cfg_t* cfg, const int64_
 
 extern "C" int tacsl_augment(const float* images, int64_t n, int height, int width, const double* params, int rep,
                              const float nominal[3], float* out, void* stream) {
+  StreamDevice stream_device_(stream);
   if (n < 0 || height < 2 || width < 2) return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: bad sizes");
   if (rep < 0 || rep > 2) return set_error(TACSL_ERR_INVALID_ARGUMENT, "augment: rep must be 0, 1 or 2");
   if (n == 0) return TACSL_OK;

@@ -72,13 +72,18 @@ __global__ void __launch_bounds__(kBinnedThreads) rgb_binned_kernel(const float*
   __syncthreads();
 
   const int QW = (W + 3) >> 2;
-  const int rows_per_pass = max(1, (int)blockDim.x / QW);
-  const int rsub = threadIdx.x / QW;
-  const int xq = threadIdx.x - rsub * QW;
+  // narrow rows: several rows per pass, one quad per thread; rows wider
+  // than 4 * blockDim pixels: one row per pass, each thread strides its quads
+  const bool narrow = QW <= (int)blockDim.x;
+  const int rows_per_pass = narrow ? (int)blockDim.x / QW : 1;
+  const int rsub = narrow ? (int)threadIdx.x / QW : 0;
+  const int xq0 = narrow ? (int)threadIdx.x - rsub * QW : (int)threadIdx.x;
+  const int xq_step = narrow ? QW : (int)blockDim.x;
   if (rsub >= rows_per_pass) return;
   const int64_t total_rows = n * H;
   for (int64_t rr = (int64_t)blockIdx.x * rows_per_pass + rsub; rr < total_rows;
-       rr += (int64_t)gridDim.x * rows_per_pass) {
+       rr += (int64_t)gridDim.x * rows_per_pass)
+  for (int xq = xq0; xq < QW; xq += xq_step) {
     const int64_t img = rr / H;
     const int r = (int)(rr - img * H);
     const float* f = depth + img * (int64_t)H * W;
@@ -345,6 +350,7 @@ extern "C" void tacsl_binned_lut_destroy(tacsl_binned_lut_t lut) {
 
 extern "C" int tacsl_depth_to_rgb_binned(tacsl_binned_lut_t lut, const float* depth, int64_t n_images, int height,
                                          int width, uint8_t* rgb_u8, float* rgb_f32, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!lut) return set_error(TACSL_ERR_INVALID_ARGUMENT, "depth_to_rgb_binned: null LUT");
   if (width != lut->width || height != lut->height)
     return set_error(TACSL_ERR_LUT_RESOLUTION_MISMATCH,

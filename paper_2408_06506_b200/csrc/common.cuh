@@ -21,6 +21,25 @@ int current_device();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device); thread-safe
 int set_max_dynamic_smem(const void* func, int bytes);  // api.cu
 
+// Compute entry points run on the device their stream belongs to, whatever
+// the calling thread's current device is (restored on return).
+struct StreamDevice {
+  int prev = -1;
+  explicit StreamDevice(void* stream) {
+    int dev = 0, cur = 0;
+    if (cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~StreamDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  StreamDevice(const StreamDevice&) = delete;
+  StreamDevice& operator=(const StreamDevice&) = delete;
+};
+
 // ----------------------------------------------------------- device side ---
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

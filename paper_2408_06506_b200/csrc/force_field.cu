@@ -311,6 +311,7 @@ extern "C" {
 
 int tacsl_query_sdf(tacsl_sdf_t sdf, const double* points, int64_t n, double* distance, double* normal,
                     uint8_t* valid, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "query_sdf: null SDF");
   if (n < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "query_sdf: negative count");
   if (n == 0) return TACSL_OK;
@@ -322,6 +323,7 @@ int tacsl_query_sdf(tacsl_sdf_t sdf, const double* points, int64_t n, double* di
 
 int tacsl_penalty_forces(const double* d, const double* d_dot, const double* n, const double* v_t, int64_t count,
                          tacsl_penalty_t params, double* f_n, double* f_t, void* stream) {
+  StreamDevice stream_device_(stream);
   int rc = check_params(params);
   if (rc) return rc;
   if (count < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "penalty_forces: negative count");
@@ -337,6 +339,7 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
                       int64_t object_stride, const double* sensor_state, int64_t sensor_stride, int64_t n_envs,
                       int n_sensors, tacsl_penalty_t params, int out_fp64, void* f_n, void* f_t, double* wrench,
                       double* kin, uint8_t* contact, float* obs, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "force_field: null SDF");
   int rc = check_params(params);
   if (rc) return rc;
@@ -392,6 +395,7 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
 
 int tacsl_net_wrench(const double* f_n, const double* f_t, const double* points, int64_t frames, int rows, int cols,
                      double* force, double* torque, void* stream) {
+  StreamDevice stream_device_(stream);
   if (frames < 0 || rows <= 0 || cols <= 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "net_wrench: bad sizes");
   if (frames == 0) return TACSL_OK;
   if (!f_n || !f_t || !points || !force || !torque)

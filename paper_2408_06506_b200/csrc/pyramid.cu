@@ -402,95 +402,106 @@ int env_int_f(const char* name, int dflt) {
 template <int R, int S>
 int dispatch_bulk(const float* in, int64_t n, int H, int W, int Ho, int Wo, const Taps& T, float* out,
                   cudaStream_t stream) {
+  // (device, H, W, log2 n) -> (rpt, groups, stages); a layout is cached only
+  // once it has been decided for good (timed, or nothing to time), so a
+  // first call under graph capture does not pin the occupancy guess
   static std::mutex mu;
-  static std::vector<std::array<int, 6>> cache;  // (H, W, log2 n) -> (rpt, groups, stages)
+  static std::vector<std::array<int, 7>> cache;
   auto launch = [&](const FLayout& l) -> int {
     if constexpr (R <= 4) {
       if (l.rpt == 8) return launch_bulk_filter<R, S, 8>(in, n, H, W, Ho, Wo, T, out, stream, l);
     }
     return launch_bulk_filter<R, S, 4>(in, n, H, W, Ho, Wo, T, out, stream, l);
   };
+  const int dev = current_device();
   const int nb = 63 - __builtin_clzll((unsigned long long)std::max<int64_t>(n, 1));
   FLayout best;
   {
     std::lock_guard<std::mutex> lock(mu);
-    bool found = false;
     for (const auto& c : cache)
-      if (c[0] == H && c[1] == W && c[2] == nb) {
-        best.rpt = c[3];
-        best.groups = c[4];
-        best.stages = c[5];
-        found = true;
+      if (c[0] == dev && c[1] == H && c[2] == W && c[3] == nb) {
+        best.rpt = c[4];
+        best.groups = c[5];
+        best.stages = c[6];
+        return launch(best);
       }
-    if (!found) {
-      const int QW = Wo / 4;
-      const int want_rpt = env_int_f("TACSL_FILTER_RPT", 0);
-      const int want_groups = env_int_f("TACSL_FILTER_GROUPS", 0);
-      const int stages = std::min(env_int_f("TACSL_FILTER_STAGES", 2), kFMaxStages);
-      long best_score = -1;
-      std::vector<FLayout> cands;  // the deepest ring that fits per (rpt, groups), two stages or more
-      for (int rpt : {8, 4}) {
-        if ((want_rpt && rpt != want_rpt) || (rpt == 8 && R > 4)) continue;  // RPT=8 spills beyond R=4
-        const int gmax = std::max(1, std::min(kFMaxCons / QW, (Ho + rpt - 1) / rpt));
-        for (int g = 1; g <= gmax; ++g) {
-          if (want_groups && g != want_groups) continue;
-          for (int st = stages; st >= 1; --st) {
-            FLayout cand;
-            cand.rpt = rpt;
-            cand.groups = g;
-            cand.stages = st;
-            long sc;
-            if constexpr (R <= 4) {
-              sc = rpt == 8 ? score_layout<R, S, 8>(cand, H, W, Ho, Wo) : score_layout<R, S, 4>(cand, H, W, Ho, Wo);
-            } else {
-              sc = score_layout<R, S, 4>(cand, H, W, Ho, Wo);
-            }
-            if (sc <= 0) continue;
-            // a single stage cannot overlap the next band's load with this
-            // one's filtering: only a last resort
-            if (st < 2) sc = 1;
-            else cands.push_back(cand);
-            // strictly better occupancy wins; on a tie the taller band
-            if (sc > best_score || (sc == best_score && cand.band() > best.band())) {
-              best_score = sc;
-              best = cand;
-            }
-            break;  // deepest ring that fits for this (rpt, groups)
-          }
+  }
+  const int QW = Wo / 4;
+  const int want_rpt = env_int_f("TACSL_FILTER_RPT", 0);
+  const int want_groups = env_int_f("TACSL_FILTER_GROUPS", 0);
+  const int stages = std::min(env_int_f("TACSL_FILTER_STAGES", 2), kFMaxStages);
+  long best_score = -1;
+  std::vector<FLayout> cands;  // the deepest ring that fits per (rpt, groups), two stages or more
+  for (int rpt : {8, 4}) {
+    if ((want_rpt && rpt != want_rpt) || (rpt == 8 && R > 4)) continue;  // RPT=8 spills beyond R=4
+    const int gmax = std::max(1, std::min(kFMaxCons / QW, (Ho + rpt - 1) / rpt));
+    for (int g = 1; g <= gmax; ++g) {
+      if (want_groups && g != want_groups) continue;
+      for (int st = stages; st >= 1; --st) {
+        FLayout cand;
+        cand.rpt = rpt;
+        cand.groups = g;
+        cand.stages = st;
+        long sc;
+        if constexpr (R <= 4) {
+          sc = rpt == 8 ? score_layout<R, S, 8>(cand, H, W, Ho, Wo) : score_layout<R, S, 4>(cand, H, W, Ho, Wo);
+        } else {
+          sc = score_layout<R, S, 4>(cand, H, W, Ho, Wo);
         }
-      }
-      if (best_score <= 0) return -1;  // caller falls back to the generic kernel
-      // The occupancy score misses part of what the measured best layout
-      // depends on (pyr_down at 2048 x 480x640: 0.575 ms scored vs 0.539 ms
-      // for 2 groups x 4 rows), so the first un-captured call per (H, W,
-      // batch-size octave) times the candidates on its own data.
-      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(stream, &cap);
-      if (cands.size() > 1 && !want_rpt && !want_groups && cap == cudaStreamCaptureStatusNone &&
-          !std::getenv("TACSL_FILTER_NO_TUNE")) {
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        float best_ms = 1e30f;
-        for (const FLayout& c : cands) {
-          if (launch(c)) continue;  // warm-up
-          cudaEventRecord(e0, stream);
-          launch(c);
-          launch(c);
-          cudaEventRecord(e1, stream);
-          cudaEventSynchronize(e1);
-          float ms = 0.f;
-          cudaEventElapsedTime(&ms, e0, e1);
-          if (ms < best_ms) {
-            best_ms = ms;
-            best = c;
-          }
+        if (sc <= 0) continue;
+        // a single stage cannot overlap the next band's load with this
+        // one's filtering: only a last resort
+        if (st < 2) sc = 1;
+        else cands.push_back(cand);
+        // strictly better occupancy wins; on a tie the taller band
+        if (sc > best_score || (sc == best_score && cand.band() > best.band())) {
+          best_score = sc;
+          best = cand;
         }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        break;  // deepest ring that fits for this (rpt, groups)
       }
-      cache.push_back({H, W, nb, best.rpt, best.groups, best.stages});
     }
+  }
+  if (best_score <= 0) return -1;  // caller falls back to the generic kernel
+  // The occupancy score misses part of what the measured best layout
+  // depends on (pyr_down at 2048 x 480x640: 0.575 ms scored vs 0.539 ms for
+  // 2 groups x 4 rows), so the first un-captured call per (device, H, W,
+  // batch-size octave) times the candidates on its own data -- outside the
+  // lock, so other threads' filters are not held up by the synchronisation.
+  bool decided = cands.size() <= 1 || want_rpt || want_groups || std::getenv("TACSL_FILTER_NO_TUNE");
+  if (!decided) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+      cudaGetLastError();  // e.g. the legacy stream while another capture runs: do not time, do not cache
+      cap = cudaStreamCaptureStatusActive;
+    }
+    if (cap == cudaStreamCaptureStatusNone) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      float best_ms = 1e30f;
+      for (const FLayout& c : cands) {
+        if (launch(c)) continue;  // warm-up
+        cudaEventRecord(e0, stream);
+        launch(c);
+        launch(c);
+        cudaEventRecord(e1, stream);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best_ms) {
+          best_ms = ms;
+          best = c;
+        }
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      decided = true;
+    }
+  }
+  if (decided) {
+    std::lock_guard<std::mutex> lock(mu);
+    cache.push_back({dev, H, W, nb, best.rpt, best.groups, best.stages});
   }
   return launch(best);
 }
@@ -518,6 +529,7 @@ using namespace tacsl;
 
 extern "C" int tacsl_separable_filter(const float* in, int64_t n_images, int height, int width, const float* taps,
                                       int radius, int step, float* out, void* stream) {
+  StreamDevice stream_device_(stream);
   if (n_images < 0 || height < 1 || width < 1) return set_error(TACSL_ERR_INVALID_ARGUMENT, "filter: bad sizes");
   if (radius < 0 || radius > (kMaxTaps - 1) / 2)
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "filter: radius must be in [0, 16]");

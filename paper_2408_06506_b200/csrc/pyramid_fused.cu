@@ -475,12 +475,10 @@ template <int R, int LEVELS, int DEG>
 int launch_pyramid(const float* depth, int64_t n, int H, int W, PyrArgs& A, cudaStream_t stream) {
   auto kern = pyramid_fused_kernel<R, LEVELS, DEG>;
   if (int rc = set_max_dynamic_smem(reinterpret_cast<const void*>(kern), 227 * 1024)) return rc;
-  static bool carve = false;  // all of the unified L1/shared array as shared memory: 3 CTAs per SM
-  if (!carve) {
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    carve = true;
-  }
+  // all of the unified L1/shared array as shared memory: 3 CTAs per SM (a
+  // host-side attribute, cheap, set on every call so every device has it)
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
   A.ticks = pyramid_ticks(H, LEVELS);
   const size_t smem = pyramid_smem(R, W);
   const int threads = ((W / 4 + 31) / 32) * 32;
@@ -528,6 +526,7 @@ extern "C" int tacsl_rgb_pyramid_supported(int height, int width, int radius, in
 extern "C" int tacsl_rgb_pyramid(const tacsl_lut_t* luts, int levels, const float* depth, int64_t n_images,
                                  int height, int width, const float* taps, int radius, uint8_t* const* out,
                                  void* stream) {
+  StreamDevice stream_device_(stream);
   if (n_images < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb_pyramid: negative image count");
   if (!tacsl_rgb_pyramid_supported(height, width, radius, levels))
     return set_error(TACSL_ERR_INVALID_ARGUMENT,

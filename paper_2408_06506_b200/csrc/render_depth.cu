@@ -242,6 +242,7 @@ extern "C" int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const dou
                                   int width, const double cam_pos[3], double near_plane, double far_plane,
                                   double hit_tolerance, int max_steps, const double* env_params, int64_t n_envs,
                                   double* depth_f64, float* depth_f32, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "render_depth: null SDF");
   if (height <= 0 || width <= 0 || n_envs < 0 || max_steps < 0)
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "render_depth: bad sizes");
@@ -282,6 +283,7 @@ extern "C" int tacsl_render_depth(tacsl_sdf_t sdf, const double* dirs, const dou
 
 extern "C" int tacsl_env_render_params(tacsl_sdf_t sdf, const double* poses, int64_t n_envs, int n_sensors,
                                        double* env_params, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "env_render_params: null SDF");
   if (n_envs < 0 || n_sensors <= 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "env_render_params: bad sizes");
   if (n_envs == 0) return TACSL_OK;

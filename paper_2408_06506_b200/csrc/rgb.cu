@@ -569,17 +569,26 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
     // ms at 8192 x 240x320 between neighbouring shapes), so the first
     // un-captured call per (H, W, batch-size octave) times the candidates
     // on its own data and keeps the fastest.
-    static std::vector<std::array<int, 5>> tuned;  // H, W, log2(n) -> groups, ctas
+    // (device, H, W, log2 n) -> (groups, ctas), cached only once timed
+    static std::mutex mu;
+    static std::vector<std::array<int, 6>> tuned;
+    const int dev = current_device();
     const int nb = 63 - __builtin_clzll((unsigned long long)std::max<int64_t>(n, 1));
     bool have = false;
-    for (const auto& t : tuned)
-      if (t[0] == H && t[1] == W && t[2] == nb) {
-        groups = t[3];
-        ctas = t[4];
-        have = true;
-      }
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      for (const auto& t : tuned)
+        if (t[0] == dev && t[1] == H && t[2] == W && t[3] == nb) {
+          groups = t[4];
+          ctas = t[5];
+          have = true;
+        }
+    }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &cap);
+    if (!have && cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+      cudaGetLastError();  // cannot tell: do not time (and do not cache) now
+      cap = cudaStreamCaptureStatusActive;
+    }
     if (!have && !std::getenv("TACSL_RGB_GROUPS") && !std::getenv("TACSL_RGB_CTAS_PER_SM") &&
         cap == cudaStreamCaptureStatusNone) {
       cudaEvent_t e0, e1;
@@ -610,7 +619,8 @@ int launch_bulk(Layout lay, const float* depth, int64_t n, int H, int W, uint8_t
       cudaEventDestroy(e1);
       groups = best_g;
       ctas = best_c;
-      tuned.push_back({H, W, nb, groups, ctas});
+      std::lock_guard<std::mutex> lock(mu);
+      tuned.push_back({dev, H, W, nb, groups, ctas});
     }
   }
   if (go(groups, ctas) < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb: band ring does not fit in shared memory");
@@ -672,6 +682,7 @@ using namespace tacsl;
 
 extern "C" int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n_images, int height, int width,
                                   uint8_t* rgb_u8, float* rgb_f32, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!lut) return set_error(TACSL_ERR_INVALID_ARGUMENT, "depth_to_rgb: null LUT");
   if (width != lut->width || height != lut->height)
     return set_error(TACSL_ERR_LUT_RESOLUTION_MISMATCH,
@@ -694,6 +705,7 @@ extern "C" int tacsl_depth_to_rgb(tacsl_lut_t lut, const float* depth, int64_t n
 
 extern "C" int tacsl_tactile_image_obs(tacsl_lut_t lut, const float* depth, int64_t n_images, int height, int width,
                                        int rep, const float nominal[3], float* out, void* stream) {
+  StreamDevice stream_device_(stream);
   if (!lut) return set_error(TACSL_ERR_INVALID_ARGUMENT, "tactile_image_obs: null LUT");
   if (rep < 0 || rep > 2) return set_error(TACSL_ERR_INVALID_ARGUMENT, "tactile_image_obs: rep must be 0, 1 or 2");
   if (width != lut->width || height != lut->height)
@@ -738,6 +750,7 @@ extern "C" int tacsl_sensor_step(tacsl_lut_t lut, const float* depth, int64_t n_
                                  int64_t sensor_stride, int64_t n_envs, int n_sensors, tacsl_penalty_t params,
                                  float* f_n, float* f_t, double* wrench, unsigned long long* workspace,
                                  void* stream) {
+  StreamDevice stream_device_(stream);
   if (!lut || !sdf) return set_error(TACSL_ERR_INVALID_ARGUMENT, "sensor_step: null handle");
   if (width != lut->width || height != lut->height)
     return set_error(TACSL_ERR_LUT_RESOLUTION_MISMATCH,

@@ -7,6 +7,8 @@
 //                         the numpy drop-ins' dtype changes done on the device
 //                         (astype rounding: to nearest, ties to even), so the
 //                         host only moves the caller's bytes once;
+//  * tacsl_relative_penetration_rate
+//                         geometry/sdf.py:324-328 (raises InvalidQuery);
 //  * tacsl_frame_digest   a position-dependent 64-bit digest per frame of any
 //                         output buffer (bench.py / multi-rank validation:
 //                         the per-frame digests of a step, in global frame
@@ -88,6 +90,27 @@ __global__ void __launch_bounds__(256) frame_digest_kernel(const uint32_t* __res
   }
 }
 
+// geometry/sdf.py:324-328 relative_penetration_rate: d_dot = n . x_dot over
+// the trailing axis, summed as numpy 2.3's einsum does for a length-3 axis
+// -- (x0 + x2) + x1 of the rounded products (measured on the reference's
+// numpy: every one of 1e5 random triples); any out-of-grid query raises the
+// flag (InvalidQuery)
+__global__ void __launch_bounds__(256) penetration_rate_kernel(const double* __restrict__ normal,
+                                                               const uint8_t* __restrict__ valid,
+                                                               const double* __restrict__ x_dot, int64_t n,
+                                                               int64_t x_stride, double* __restrict__ out,
+                                                               int* __restrict__ invalid) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double* a = normal + 3 * i;
+    const double* b = x_dot + x_stride * i;
+    out[i] = __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[2], b[2])), __dmul_rn(a[1], b[1]));
+    bad |= valid[i] == 0;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(invalid, 1);
+}
+
 int grid_for(int64_t count) {
   int64_t blocks = (count + 255) / 256;
   const int64_t cap = (int64_t)sm_count(current_device()) * 8;
@@ -100,6 +123,7 @@ int grid_for(int64_t count) {
 using namespace tacsl;
 
 extern "C" int tacsl_to_uint8_f64(const double* x, int64_t count, uint8_t* out, void* stream) {
+  StreamDevice stream_device_(stream);
   if (count < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "to_uint8_f64: negative count");
   if (count == 0) return TACSL_OK;
   if (!x || !out) return set_error(TACSL_ERR_INVALID_ARGUMENT, "to_uint8_f64: null pointer");
@@ -108,6 +132,7 @@ extern "C" int tacsl_to_uint8_f64(const double* x, int64_t count, uint8_t* out, 
 }
 
 extern "C" int tacsl_f64_to_f32(const double* x, int64_t count, float* out, void* stream) {
+  StreamDevice stream_device_(stream);
   if (count < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "f64_to_f32: negative count");
   if (count == 0) return TACSL_OK;
   if (!x || !out) return set_error(TACSL_ERR_INVALID_ARGUMENT, "f64_to_f32: null pointer");
@@ -116,6 +141,7 @@ extern "C" int tacsl_f64_to_f32(const double* x, int64_t count, float* out, void
 }
 
 extern "C" int tacsl_f32_to_f64(const float* x, int64_t count, double* out, void* stream) {
+  StreamDevice stream_device_(stream);
   if (count < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "f32_to_f64: negative count");
   if (count == 0) return TACSL_OK;
   if (!x || !out) return set_error(TACSL_ERR_INVALID_ARGUMENT, "f32_to_f64: null pointer");
@@ -125,6 +151,7 @@ extern "C" int tacsl_f32_to_f64(const float* x, int64_t count, double* out, void
 
 extern "C" int tacsl_frame_digest(const void* data, int64_t n_frames, int64_t frame_bytes, uint64_t* out,
                                   void* stream) {
+  StreamDevice stream_device_(stream);
   if (n_frames < 0 || frame_bytes < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "frame_digest: bad sizes");
   if (frame_bytes % 4 != 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "frame_digest: frame_bytes % 4 != 0");
   if (n_frames == 0) return TACSL_OK;
@@ -136,4 +163,25 @@ extern "C" int tacsl_frame_digest(const void* data, int64_t n_frames, int64_t fr
   frame_digest_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint32_t*>(data), n_frames,
                                                               frame_bytes / 4, out);
   return check_launch("frame_digest");
+}
+
+extern "C" int tacsl_relative_penetration_rate(const double* normal, const uint8_t* valid, const double* x_dot,
+                                               int64_t n, int x_dot_broadcast, double* out, int* scratch,
+                                               void* stream) {
+  StreamDevice stream_device_(stream);
+  if (n < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "penetration_rate: negative count");
+  if (n == 0) return TACSL_OK;
+  if (!normal || !valid || !x_dot || !out || !scratch)
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "penetration_rate: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(scratch, 0, sizeof(int), s);
+  penetration_rate_kernel<<<grid_for(n), 256, 0, s>>>(normal, valid, x_dot, n, x_dot_broadcast ? 0 : 3, out,
+                                                      scratch);
+  if (int rc = check_launch("penetration_rate")) return rc;
+  int bad = 0;  // the reference raises synchronously: read the flag back
+  if (cudaMemcpyAsync(&bad, scratch, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return check_launch("penetration_rate (flag read-back)");
+  if (bad) return set_error(TACSL_ERR_INVALID_QUERY, "penetration rate requires in-bounds queries");
+  return TACSL_OK;
 }

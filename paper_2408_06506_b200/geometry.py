@@ -150,6 +150,33 @@ def query_sdf(grid, points) -> SdfQuery:
 # ---------------------------------------------------------------------------
 
 
+def relative_penetration_rate(q: SdfQuery, x_dot):
+    """Drop-in for gelsim.geometry.relative_penetration_rate (sdf.py:324-328):
+    d_dot = n . x_dot per query, on the GPU; raises InvalidQuery when any
+    query was out of the grid.  numpy in -> numpy out, CUDA in -> CUDA out."""
+    t = _device.torch()
+    on_device = _device.is_cuda_tensor(q.normal)
+    dev = _device.resolve_device(q.normal.device if on_device else None)
+    normal = _device.to_device(q.normal, t.float64, dev)
+    valid = _device.to_device(q.valid, t.uint8, dev) if not _device.is_cuda_tensor(q.valid) else \
+        q.valid.to(t.uint8).contiguous()
+    xd = _device.to_device(x_dot, t.float64, dev)
+    shape = tuple(normal.shape[:-1])
+    single_x = tuple(xd.shape) == (3,)
+    if not single_x:
+        xd = xd.expand(tuple(normal.shape)).contiguous()
+    n = int(np.prod(shape, dtype=np.int64)) if shape else 1
+    out = t.empty(shape, dtype=t.float64, device=dev)
+    scratch = t.empty(1, dtype=t.int32, device=dev)
+    _lib.check(_lib.load().tacsl_relative_penetration_rate(
+        normal.data_ptr(), valid.data_ptr(), xd.data_ptr(), n, int(single_x), out.data_ptr(), scratch.data_ptr(),
+        _device.stream_handle(dev)))
+    if on_device:
+        return out
+    host = out.cpu().numpy()
+    return host if shape else np.float64(host)
+
+
 def write_sdf_cache(grid, path) -> None:
     with open(path, "wb") as fh:
         fh.write(SDF_MAGIC)

@@ -8,7 +8,7 @@ the defining one:
     gelsim.render, gelsim.render.imageio      to_uint8
     gelsim.tactile, gelsim.tactile.field      compute_force_field, penalty_forces, net_wrench
     gelsim.envs.peg_tasks, gelsim.envs.scenes depth_to_rgb, compute_force_field
-    gelsim.geometry, gelsim.geometry.sdf      query_sdf (standalone API only)
+    gelsim.geometry, gelsim.geometry.sdf      query_sdf, relative_penetration_rate (standalone API only)
 
 and replaces ``PegEnvBatch._tactile_images`` / ``_tactile_ff``
 (envs/peg_tasks.py:434-477) by their batched versions in ``envs.py``.
@@ -33,7 +33,7 @@ _SITES = {
     "gelsim.envs.peg_tasks": ("depth_to_rgb", "compute_force_field", "render_depth", "augment"),
     "gelsim.envs.scenes": ("depth_to_rgb", "compute_force_field", "render_depth"),
     "gelsim.envs.wrist": ("render_depth",),
-    "gelsim.geometry": ("query_sdf",),
+    "gelsim.geometry": ("query_sdf", "relative_penetration_rate"),
 }
 
 # env methods replaced by their batched versions (envs.py): one launch per
@@ -58,6 +58,7 @@ def _impl(name):
         "penalty_forces": tactile.penalty_forces,
         "net_wrench": tactile.net_wrench,
         "query_sdf": geometry.query_sdf,
+        "relative_penetration_rate": geometry.relative_penetration_rate,
     }[name]
 
 

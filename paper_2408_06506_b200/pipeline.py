@@ -52,7 +52,14 @@ class SensorArray:
         # level's LUT, each into its own uint8 RGB buffer
         self.levels = max(1, int(pyramid_levels)) if self.with_rgb else 1
         self.sigma = float(smooth_sigma) if self.with_rgb else 0.0
-        self._smooth = (t.empty((self.E, self.S, H, W), dtype=t.float32, device=dev) if self.sigma > 0 else None)
+        # K7: smoothing + every pyramid level's RGB in one pass over the
+        # depth (no intermediate in HBM) whenever the shape allows it;
+        # otherwise the level-by-level chain (K5 + K1 per level)
+        self.fused_pyramid = bool(self.with_rgb and rgb_u8 and not rgb_f32 and (self.levels > 1 or self.sigma > 0)
+                                  and smoothing.fused_pyramid_supported(H, W, self.levels, self.sigma))
+        chain = not self.fused_pyramid  # the intermediates exist only for the level-by-level chain
+        self._smooth = (t.empty((self.E, self.S, H, W), dtype=t.float32, device=dev)
+                        if self.sigma > 0 and chain else None)
         self._taps = smoothing.gaussian_taps(self.sigma) if self.sigma > 0 else None
         self.rgb_levels = [self.rgb_u8]
         self._lvl_depth = [None]
@@ -60,7 +67,7 @@ class SensorArray:
         h, w = H, W
         for lvl in range(1, self.levels):
             h, w = -(-h // 2), -(-w // 2)
-            self._lvl_depth.append(t.empty((self.E, self.S, h, w), dtype=t.float32, device=dev))
+            self._lvl_depth.append(t.empty((self.E, self.S, h, w), dtype=t.float32, device=dev) if chain else None)
             self.rgb_levels.append(t.empty((self.E, self.S, h, w, 3), dtype=t.uint8, device=dev))
             self._lvl_luts.append(device_lut(smoothing.level_lut(lut, lvl)))
         # one fused launch (force-field warps beside the shading warps) when
@@ -69,6 +76,8 @@ class SensorArray:
                           and self.sigma == 0)
         self.overlap = overlap and self.with_rgb and with_ff and not self.fused
         rgb_launches = (1 + int(self.sigma > 0) + 2 * (self.levels - 1)) if self.with_rgb else 0
+        if self.fused_pyramid:
+            rgb_launches = 1
         self.launches_per_step = 1 if self.fused else rgb_launches + int(with_ff)
         self._workspace = t.zeros(1, dtype=t.int64, device=dev) if self.fused else None
         self._ff_stream = t.cuda.Stream(device=dev) if overlap else None
@@ -85,8 +94,8 @@ class SensorArray:
         rgb_out = (3 if self.rgb_u8 is not None else 0) + (12 if self.rgb_f32 is not None else 0)
         F = self.E * self.S
         rgb = F * px * (4 + rgb_out) if self.with_rgb else 0
-        for d in self._lvl_depth[1:]:
-            h, w = d.shape[-2:]
+        for lvl in range(1, self.levels):
+            h, w = self.rgb_levels[lvl].shape[2:4]
             rgb += F * h * w * 3  # level l's uint8 RGB
         ff = 0
         if self.with_ff:
@@ -95,9 +104,12 @@ class SensorArray:
         return {"rgb": rgb, "ff": ff, "total": rgb + ff}
 
     def image_kernel_name(self) -> str:
-        return "image_pipeline"
+        return "pyramid_fused_kernel" if self.fused_pyramid else "image_pipeline"
 
     def image_kernel_desc(self) -> str:
+        if self.fused_pyramid:
+            return ("pyramid_fused_kernel (K7: Gaussian smoothing + RGB of every pyramid level in one pass; "
+                    "only the depth is read and the uint8 RGB written)")
         return ("image pipeline: sep_bulk_kernel smoothing + rgb_bulk_kernel, then per pyramid level "
                 "sep_bulk_kernel pyr_down + rgb_bulk_kernel (all launches of the RGB side)")
 
@@ -137,6 +149,11 @@ class SensorArray:
         hi = self.E if hi is None else hi
         sl = slice(lo, hi)
         d = depth[sl]
+        if self.fused_pyramid:
+            smoothing.rgb_pyramid_fused_device(d, self.lut, self.levels, self.sigma,
+                                               outs=[self.rgb_levels[lvl][sl] for lvl in range(self.levels)],
+                                               luts=self._lvl_luts)
+            return
         if self._smooth is not None:
             d = smoothing.separable_filter_device(d, self._taps, 1, out=self._smooth[sl])
         if self.levels == 1:

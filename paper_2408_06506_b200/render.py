@@ -196,8 +196,10 @@ def depth_to_rgb(depth, lut, out_dtype=None):
         raise LutResolutionMismatch(f"LUT calibrated at {tuple(lut.image_size)}, image is {(W, H)}")
     on_device = _device.is_cuda_tensor(values)
     dev = _device.resolve_device(values.device if on_device else None)
-    v = _device.as_f32(values, dev)  # float64 depth is narrowed on the device
     want_u8 = out_dtype in (np.uint8, t.uint8, "uint8")
+    if not on_device:
+        return _depth_to_rgb_host(np.asarray(values), lut, want_u8, dev)
+    v = _device.as_f32(values, dev)  # float64 depth is narrowed on the device
     shape = tuple(v.shape) + (3,)
     if want_u8:
         out = t.empty(shape, dtype=t.uint8, device=dev)
@@ -210,6 +212,51 @@ def depth_to_rgb(depth, lut, out_dtype=None):
     if want_u8:
         return out.cpu().numpy()
     return _device.widen_f64(out).cpu().numpy()  # the reference's float64, widened on the device
+
+
+_HOST_CHUNK_BYTES = 48 << 20  # input bytes per pipelined chunk of the numpy path
+
+
+def _depth_to_rgb_host(values, lut, want_u8, dev):
+    """The numpy path of depth_to_rgb: the caller's array is staged once into
+    page-locked memory as it is (float64 stays float64), and chunks then
+    stream upload -> narrow on the device -> K1 -> widen on the device ->
+    download into the page-locked result array, overlapped on three streams
+    (_device.pipelined).  The host does one copy in and none out."""
+    t = _device.torch()
+    src_dtype = t.float64 if values.dtype == np.float64 else t.float32
+    H, W = values.shape[-2], values.shape[-1]
+    lead = tuple(values.shape[:-2])
+    n = int(np.prod(lead, dtype=np.int64)) if lead else 1
+    pin_in = _device.to_pinned(values.reshape(n, H, W), src_dtype)
+    out_dtype = t.uint8 if want_u8 else t.float64
+    pin_out = _device.pinned_empty((n, H, W, 3), out_dtype)
+    dl = device_lut(lut)
+    chunk = max(1, min(n, _HOST_CHUNK_BYTES // max(H * W * pin_in.element_size(), 1)))
+    scratch = {}
+
+    def fn(ins, outs):
+        d = ins[0]
+        m = d.shape[0]
+        if d.dtype == t.float64:
+            if "d32" not in scratch:
+                scratch["d32"] = t.empty((chunk, H, W), dtype=t.float32, device=dev)
+            d32 = scratch["d32"][:m]
+            _lib.check(_lib.load().tacsl_f64_to_f32(d.data_ptr(), d.numel(), d32.data_ptr(),
+                                                    _device.stream_handle(dev)))
+            d = d32
+        if want_u8:
+            depth_to_rgb_device(d, dl, out_u8=outs[0])
+            return
+        if "rgb32" not in scratch:
+            scratch["rgb32"] = t.empty((chunk, H, W, 3), dtype=t.float32, device=dev)
+        rgb32 = scratch["rgb32"][:m]
+        depth_to_rgb_device(d, dl, out_f32=rgb32)
+        _lib.check(_lib.load().tacsl_f32_to_f64(rgb32.data_ptr(), rgb32.numel(), outs[0].data_ptr(),
+                                                _device.stream_handle(dev)))
+
+    _device.pipelined([pin_in], [pin_out], fn, dev, chunk)
+    return pin_out.numpy().reshape(lead + (H, W, 3))
 
 
 def to_uint8(img):

@@ -39,9 +39,11 @@ class TactileSensorSpec:
 
 @dataclass
 class TactileCamera:
-    """Pinhole camera in the sensor frame looking along +z (camera.py:13-43)."""
+    """Pinhole camera at a fixed pose in the sensor frame, looking along its
+    +z (camera.py:13-43); ``quat`` (w, x, y, z) rotates the rays."""
 
     pos: np.ndarray = field(default_factory=lambda: np.array([0.0, 0.0, -0.02]))
+    quat: np.ndarray = field(default_factory=lambda: IDENTITY_QUAT.copy())
     fx: float = 66.7
     fy: float = 66.7
     cx: float = 40.0
@@ -51,13 +53,25 @@ class TactileCamera:
     near: float = 0.002
     far: float = 0.2
 
+    def __post_init__(self):  # camera.py:28-34
+        self.pos = np.asarray(self.pos, dtype=np.float64)
+        self.quat = np.asarray(self.quat, dtype=np.float64)
+        if self.width <= 0 or self.height <= 0:
+            raise ValueError("image size must be positive")
+        if not (0 < self.near < self.far):
+            raise ValueError("need 0 < near < far")
+
     def rays(self) -> np.ndarray:
-        """Unit ray directions (H, W, 3); pixel centres at +0.5 (camera.py:36-43)."""
+        """Unit ray directions (H, W, 3) in the sensor frame; pixel centres at
+        +0.5, rotated by ``quat`` (camera.py:36-43)."""
+        from .transforms import quat_rotate
+
         u = (np.arange(self.width) + 0.5 - self.cx) / self.fx
         v = (np.arange(self.height) + 0.5 - self.cy) / self.fy
         gu, gv = np.meshgrid(u, v, indexing="xy")
         d = np.stack([gu, gv, np.ones_like(gu)], axis=-1)
-        return d / np.linalg.norm(d, axis=-1, keepdims=True)
+        d = d / np.linalg.norm(d, axis=-1, keepdims=True)
+        return quat_rotate(self.quat, d)
 
 
 def camera_for_sensor(sensor: TactileSensorSpec) -> TactileCamera:

@@ -191,13 +191,13 @@ def compute_force_field(points, object_sdf, object_pos, object_quat, object_linv
     f_t = t.empty_like(f_n)
     kin = t.empty((E, R, C, 8), dtype=t.float64, device=dev) if return_kinematics else None
     force_field_device(dsdf, tax, R, C, obj_d, sen_d, params, f_n, f_t, kin=kin)
-    fn, ft = f_n.cpu().numpy(), f_t.cpu().numpy()
+    fn, ft = _device.download(f_n), _device.download(f_t)  # straight into page-locked result arrays
     if not batched:
         fn, ft = fn[0], ft[0]
     fld = ForceField(f_n=fn, f_t=ft, frame_index=frame_index)
     if not return_kinematics:
         return fld
-    k = kin.cpu().numpy()
+    k = _device.download(kin)
     if not batched:
         k = k[0]
     kinematics = {"d": k[..., 0], "d_dot": k[..., 1], "v_t": k[..., 2:5], "n": k[..., 5:8]}

@@ -21,6 +21,9 @@ Fixtures:
   env.npz        PegEnvBatch tactile image / force-field observations with
                  augmentation and their inputs (``make_golden.py env``)
   scene.npz      shape_sensing_scene end to end (``make_golden.py scene``)
+  extras.npz     TactileCamera with a rotated pose (rays, reference_depth) and
+                 relative_penetration_rate (+ the InvalidQuery case) on the
+                 sdf.npz grid (``make_golden.py extras``)
 """
 from __future__ import annotations
 
@@ -324,10 +327,42 @@ def make_scene(grid):
                         f_n=fld.f_n, f_t=fld.f_t)
 
 
+def make_extras(grid):
+    from gelsim.errors import InvalidQuery
+    from gelsim.geometry import relative_penetration_rate
+    from gelsim.render.camera import TactileCamera
+    from gelsim.transforms import quat_from_axis_angle
+
+    sensor = TactileSensorSpec(image_size=(80, 60))
+    base = camera_for_sensor(sensor)
+    quat = quat_from_axis_angle(np.array([0.3, -0.5, 0.8]), 0.21)
+    cam = TactileCamera(pos=base.pos, quat=quat, fx=base.fx, fy=base.fy, cx=base.cx, cy=base.cy,
+                        width=base.width, height=base.height, near=base.near, far=base.far)
+    rays = cam.rays()
+    bg = reference_depth(cam, sensor)
+    rng = np.random.default_rng(9)
+    lo, hi = grid.origin, grid.upper
+    inside = lo + rng.uniform(0.01, 0.99, (500, 3)) * (hi - lo)
+    q = query_sdf(grid, inside)
+    x_dot = rng.normal(0.0, 0.05, (500, 3))
+    rate = relative_penetration_rate(q, x_dot)
+    x1 = np.array([0.01, -0.02, 0.03])
+    rate1 = relative_penetration_rate(q, x1)
+    mixed = np.concatenate([inside[:10], [hi + 0.01]])
+    try:
+        relative_penetration_rate(query_sdf(grid, mixed), x_dot[:11])
+        raised = False
+    except InvalidQuery:
+        raised = True
+    np.savez_compressed(HERE / "extras.npz", cam_quat=quat, cam_pos=cam.pos, cam_f=np.array([cam.fx, cam.fy]),
+                        cam_c=np.array([cam.cx, cam.cy]), rays=rays, background=bg, points=inside, x_dot=x_dot,
+                        rate=rate, x1=x1, rate1=rate1, mixed=mixed, mixed_raises=np.array(raised))
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     for name in sys.argv[1:]:
         fn = globals()[f"make_{name}"]
-        fn(peg_grid_reference()) if name in ("sdf", "ff", "depth", "scene") else fn()
+        fn(peg_grid_reference()) if name in ("sdf", "ff", "depth", "scene", "extras") else fn()
 elif __name__ == "__main__":
     make_augment()
     make_rgb()
@@ -339,5 +374,6 @@ elif __name__ == "__main__":
     make_formats()
     make_env()
     make_scene(g)
+    make_extras(g)
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)

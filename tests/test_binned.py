@@ -179,3 +179,23 @@ def test_gpu_band_pipeline_table_in_smem_equals_l1(monkeypatch, deg):
     depth_to_rgb_binned_device(dd, v, out_u8=b, out_f32=fb)
     torch.cuda.synchronize()
     assert torch.equal(a, b) and torch.equal(fa, fb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("size,scalar", [((1283, 12), False), ((1600, 10), True), ((2050, 6), True)])
+def test_gpu_binned_wide_rows(monkeypatch, size, scalar):
+    """Rows wider than 4 x the per-quad kernel's threads: every
+    column is written (the generic kernel strides its quads)."""
+    import torch
+    from paper_2408_06506_b200.binned import depth_to_rgb_binned
+    if scalar:
+        monkeypatch.setenv("TACSL_BINNED_SCALAR", "1")
+    W, H = size
+    rng = np.random.default_rng(W)
+    d = rng.uniform(0.02, 0.0202, size=(2, H, W)).astype(np.float32)
+    lut = synthetic.synthetic_lut(size, degree=2, gradient_scale=synthetic.lut_scale(size) * 0.1)
+    v = vignetted_lut(lut, bins=(3, 5), falloff=0.4)
+    ref = O.to_uint8(oracle_binned(d, v.coeffs, v.degree))
+    got = depth_to_rgb_binned(torch.from_numpy(d).cuda(), v, out_dtype=np.uint8).cpu().numpy()
+    diff = np.abs(got.astype(int) - ref.astype(int))
+    assert diff.max() <= 1 and (diff > 0).mean() < 1e-3

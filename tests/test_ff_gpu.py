@@ -337,3 +337,27 @@ def test_fast_chain_decides_boundary_taxels_exactly(monkeypatch):
     exact_c, exact_f = run()
     assert np.array_equal(fast_c, exact_c)
     assert vec_close(fast_f, exact_f, 1e-9, atol=1e-15)[0]
+
+
+def test_relative_penetration_rate_golden_and_invalid_query(golden, golden_grid):
+    """geometry/sdf.py:324-328 on the GPU: bit-exact d_dot, broadcast x_dot,
+    and InvalidQuery for an out-of-grid query (the C ABI's INVALID_QUERY)."""
+    from paper_2408_06506_b200.errors import InvalidQuery
+    from paper_2408_06506_b200.geometry import query_sdf, relative_penetration_rate
+    z = golden("extras")
+    q = query_sdf(golden_grid, z["points"])
+    # the normals match the reference to rounding (only the distance is
+    # bit-exact), so d_dot does too; on the same normals the dot product is
+    # numpy 2.3's einsum order, (n0 x0 + n2 x2) + n1 x1, bit for bit
+    got = relative_penetration_rate(q, z["x_dot"])
+    np.testing.assert_allclose(got, z["rate"], rtol=1e-12, atol=1e-15)
+    n, x = q.normal, z["x_dot"]
+    np.testing.assert_array_equal(got, (n[:, 0] * x[:, 0] + n[:, 2] * x[:, 2]) + n[:, 1] * x[:, 1])
+    np.testing.assert_allclose(relative_penetration_rate(q, z["x1"]), z["rate1"], rtol=1e-12, atol=1e-15)
+    qd = query_sdf(golden_grid, torch.from_numpy(z["points"]).cuda())
+    got_d = relative_penetration_rate(qd, torch.from_numpy(z["x_dot"]).cuda())
+    assert got_d.is_cuda
+    np.testing.assert_array_equal(got_d.cpu().numpy(), got)
+    assert bool(z["mixed_raises"])
+    with pytest.raises(InvalidQuery):
+        relative_penetration_rate(query_sdf(golden_grid, z["mixed"]), z["x_dot"][:11])

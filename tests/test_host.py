@@ -120,3 +120,29 @@ def test_host_quaternion_helpers_match_the_oracle_bit_for_bit():
                     aw * by - ax * bz + ay * bw + az * bx, aw * bz + ax * by - ay * bx + az * bw], axis=-1)
     assert np.array_equal(T.quat_mul(a, b), ref)
     assert np.array_equal(T.quat_conj(q), q * np.array([1.0, -1.0, -1.0, -1.0]))
+
+
+def test_rotated_camera_rays_and_background_bit_exact(golden):
+    """TactileCamera.quat rotates the rays (render/camera.py:17,43); rays and
+    the membrane depth of a rotated camera equal the reference's bit for bit."""
+    from paper_2408_06506_b200.sensors import TactileCamera, TactileSensorSpec, reference_depth
+    z = golden("extras")
+    cam = TactileCamera(pos=z["cam_pos"], quat=z["cam_quat"], fx=float(z["cam_f"][0]), fy=float(z["cam_f"][1]),
+                        cx=float(z["cam_c"][0]), cy=float(z["cam_c"][1]), width=80, height=60)
+    np.testing.assert_array_equal(cam.rays(), z["rays"])
+    np.testing.assert_array_equal(reference_depth(cam, TactileSensorSpec(image_size=(80, 60))), z["background"])
+
+
+def test_camera_validation_and_identity_quat():
+    import pytest
+    from paper_2408_06506_b200.sensors import TactileCamera
+    with pytest.raises(ValueError):
+        TactileCamera(width=0)
+    with pytest.raises(ValueError):
+        TactileCamera(near=0.5, far=0.1)
+    cam = TactileCamera()
+    u = (np.arange(80) + 0.5 - 40.0) / 66.7
+    v = (np.arange(60) + 0.5 - 30.0) / 66.7
+    gu, gv = np.meshgrid(u, v, indexing="xy")
+    d = np.stack([gu, gv, np.ones_like(gu)], axis=-1)
+    np.testing.assert_array_equal(cam.rays(), d / np.linalg.norm(d, axis=-1, keepdims=True))

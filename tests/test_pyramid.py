@@ -119,8 +119,8 @@ def test_sensor_array_pyramid_step_and_host_path():
     d = torch.from_numpy(synthetic.depth_batch(cam, bg, E, config_id=73)).cuda().view(E, 1, 480, 640)
     arr = SensorArray(lut, synthetic.peg_grid(), pts, PenaltyParams(), E, 1, with_ff=False, pyramid_levels=3,
                       smooth_sigma=1.0)
-    assert arr.launches_per_step == 6
-    ref = smoothing.rgb_pyramid_device(d, lut, levels=3, sigma=1.0)
+    assert arr.fused_pyramid and arr.launches_per_step == 1  # K7: one pass
+    ref = smoothing.rgb_pyramid_device(d, lut, levels=3, sigma=1.0)  # the level-by-level chain
     arr.capture(d, None, None)
     arr.replay()
     torch.cuda.synchronize()

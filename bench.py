@@ -644,8 +644,9 @@ def main():
                     senF[:, 0:3], senF[:, 3:7], senF[:, 7:10], senF[:, 10:13], c.params)
             return out
 
-        for _ in range(2):
-            call()
+        out = None
+        for _ in range(3):  # warm with the timed loop's pattern (the previous result alive during a call)
+            out = call()
         reps = max(2, args.e2e_steps // 2)
         barrier()
         t0 = time.perf_counter()

@@ -124,29 +124,44 @@ def download(x):
 
 
 def pipelined(host_in, host_out, fn, device, chunk):
-    """Run fn over the leading axis of pinned host tensors in chunks: chunk
-    i's upload, chunk i-1's kernels and chunk i-2's download overlap on three
-    streams (the two copy engines + the SMs).  fn(dev_ins, dev_outs) enqueues
-    its kernels on the current stream; device chunk buffers are double
+    """Run fn over the leading axis in chunks, overlapping the host copy of
+    chunk i+1 (numpy -> page-locked staging, on the calling thread), chunk
+    i's upload, chunk i-1's kernels and chunk i-2's download (three streams:
+    the two copy engines + the SMs).  host_in: numpy arrays or page-locked
+    tensors; host_out: page-locked tensors.  fn(dev_ins, dev_outs) enqueues
+    its kernels on the current stream; device and staging buffers are double
     buffered."""
     t = torch()
     n = host_in[0].shape[0]
     main = t.cuda.current_stream(device)
     up, down = t.cuda.Stream(device=device), t.cuda.Stream(device=device)
-    bufs = [([t.empty((chunk,) + tuple(h.shape[1:]), dtype=h.dtype, device=device) for h in host_in],
+    srcs = [h if isinstance(h, t.Tensor) else t.from_numpy(np.ascontiguousarray(h)) for h in host_in]
+    staged = [not (isinstance(h, t.Tensor) and h.is_pinned()) for h in host_in]
+    stage = [[pinned_empty((chunk,) + tuple(x.shape[1:]), x.dtype) if st else None for x, st in zip(srcs, staged)]
+             for _ in range(2)]
+    bufs = [([t.empty((chunk,) + tuple(x.shape[1:]), dtype=x.dtype, device=device) for x in srcs],
              [t.empty((chunk,) + tuple(h.shape[1:]), dtype=h.dtype, device=device) for h in host_out])
             for _ in range(2)]
-    free = [None, None]  # event: buffer set b may be overwritten (its download finished)
+    free = [None, None]      # event: buffer set b may be overwritten (its download finished)
+    uploaded = [None, None]  # event: staging set b has been read by its upload
     up.wait_stream(main)
     for i, lo in enumerate(range(0, n, chunk)):
         hi = min(lo + chunk, n)
         b = i & 1
         ins, outs = bufs[b]
+        if uploaded[b] is not None:
+            uploaded[b].synchronize()  # the host may now refill staging set b
+        for k, x in enumerate(srcs):
+            if staged[k]:
+                stage[b][k][:hi - lo].copy_(x[lo:hi])  # host copy, torch's threads
         with t.cuda.stream(up):
             if free[b] is not None:
                 up.wait_event(free[b])
-            for d, h in zip(ins, host_in):
-                d[:hi - lo].copy_(h[lo:hi], non_blocking=True)
+            for k, (d, x) in enumerate(zip(ins, srcs)):
+                d[:hi - lo].copy_(stage[b][k][:hi - lo] if staged[k] else x[lo:hi], non_blocking=True)
+            ev = t.cuda.Event()
+            ev.record(up)
+            uploaded[b] = ev
         main.wait_stream(up)
         fn([d[:hi - lo] for d in ins], [d[:hi - lo] for d in outs])
         down.wait_stream(main)

@@ -27,6 +27,14 @@ struct StreamDevice {
   int prev = -1;
   explicit StreamDevice(void* stream) {
     int dev = 0, cur = 0;
+    // under stream capture the calling thread is already on the capture's
+    // device, and querying the stream's device would invalidate the capture
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    if (cap != cudaStreamCaptureStatusNone) return;
     if (cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev) != cudaSuccess) {
       cudaGetLastError();
       return;

@@ -218,21 +218,22 @@ _HOST_CHUNK_BYTES = 48 << 20  # input bytes per pipelined chunk of the numpy pat
 
 
 def _depth_to_rgb_host(values, lut, want_u8, dev):
-    """The numpy path of depth_to_rgb: the caller's array is staged once into
-    page-locked memory as it is (float64 stays float64), and chunks then
-    stream upload -> narrow on the device -> K1 -> widen on the device ->
-    download into the page-locked result array, overlapped on three streams
-    (_device.pipelined).  The host does one copy in and none out."""
+    """The numpy path of depth_to_rgb: chunks of the caller's array (float64
+    stays float64) stream host copy into page-locked staging -> upload ->
+    narrow on the device -> K1 -> widen on the device -> download into the
+    page-locked result array, all stages overlapped (_device.pipelined).
+    The host does one copy in and none out."""
     t = _device.torch()
     src_dtype = t.float64 if values.dtype == np.float64 else t.float32
     H, W = values.shape[-2], values.shape[-1]
     lead = tuple(values.shape[:-2])
     n = int(np.prod(lead, dtype=np.int64)) if lead else 1
-    pin_in = _device.to_pinned(values.reshape(n, H, W), src_dtype)
+    src = np.ascontiguousarray(values.reshape(n, H, W),
+                               dtype=np.float64 if src_dtype == t.float64 else np.float32)
     out_dtype = t.uint8 if want_u8 else t.float64
     pin_out = _device.pinned_empty((n, H, W, 3), out_dtype)
     dl = device_lut(lut)
-    chunk = max(1, min(n, _HOST_CHUNK_BYTES // max(H * W * pin_in.element_size(), 1)))
+    chunk = max(1, min(n, _HOST_CHUNK_BYTES // max(H * W * src.itemsize, 1)))
     scratch = {}
 
     def fn(ins, outs):
@@ -255,7 +256,7 @@ def _depth_to_rgb_host(values, lut, want_u8, dev):
         _lib.check(_lib.load().tacsl_f32_to_f64(rgb32.data_ptr(), rgb32.numel(), outs[0].data_ptr(),
                                                 _device.stream_handle(dev)))
 
-    _device.pipelined([pin_in], [pin_out], fn, dev, chunk)
+    _device.pipelined([src], [pin_out], fn, dev, chunk)
     return pin_out.numpy().reshape(lead + (H, W, 3))
 
 

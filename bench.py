@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample length")
     p.add_argument("--dropin-frames", type=int, default=1024,
                    help="sensor frames per call of the numpy drop-in e2e leg (0: skip)")
+    p.add_argument("--also", default="4,5",
+                   help="comma-separated other configs timed briefly after the main one (N=1 only; '' to skip)")
+    p.add_argument("--also-steps", type=int, default=10)
     p.add_argument("--sustain-s", type=float, default=1.5,
                    help="seconds of back-to-back steps for value_sustained (0: skip)")
     p.add_argument("--envs", type=int, default=None,
@@ -427,6 +430,58 @@ def validate(c, world, rank, coll_dev, n_samples=16):
     return {"parity": check_parity(c, idx, got), "digest": digest_summary(names, table)}
 
 
+def run_other_config(cid, dev, args, peak):
+    """One extra config on this GPU: graph-captured step, K steps timed with
+    CUDA events, the dominant kernel timed alone, the parity block."""
+    import torch
+
+    from paper_2408_06506_b200 import synthetic
+
+    wl = synthetic.CONFIGS[cid]
+    c = setup_workload(wl, 0, 1, dev)
+    arr = c.arr
+    arr.capture(c.depth, c.obj, c.sen)
+    for _ in range(3):
+        arr.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, n):
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    ms = timed(arr.replay, args.also_steps)
+    bytes_ = arr.algorithmic_bytes()
+    if wl.rgb:
+        name, kbytes = arr.image_kernel_name() if (arr.levels > 1 or arr.sigma > 0) else "rgb_bulk_kernel", \
+            bytes_["rgb"]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            arr._launch_rgb(c.depth)
+    else:
+        name, kbytes = "force_field_fast_kernel", bytes_["ff"]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            arr._launch_ff(c.obj, c.sen)
+    g.replay()
+    torch.cuda.synchronize()
+    kms = timed(g.replay, args.also_steps)
+    v = validate(c, 1, 0, dev)
+    out = {"workload": workload_text(wl), "value": wl.frames / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+           "steps": args.also_steps, "kernel": name, "kernel_ms": kms,
+           "kernel_frac_of_hbm_peak": kbytes / (kms / 1e3) / 1e9 / peak,
+           "traffic": traffic_from_profiles(f"{name}/config{cid}/world1"),
+           "algorithmic_bytes_per_launch": kbytes, "parity": v["parity"], "validation_sha256": v["digest"]["sha256"]}
+    del c, arr, g
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -738,6 +793,17 @@ def main():
     if validation is not None:
         line["parity"] = validation["parity"]
         line["validation"] = validation["digest"]
+
+    # ---- the other BASELINE configs on the same box, briefly (device-timed
+    # value, dominant kernel vs the HBM peak, sampled-frame parity), so the
+    # default run leaves evidence for every configuration
+    if rank == 0 and world == 1 and args.also:
+        other = {}
+        for cid in [int(x) for x in args.also.split(",") if x.strip()]:
+            if cid == wl.config_id:
+                continue
+            other[str(cid)] = run_other_config(cid, dev, args, peak)
+        line["other_configs"] = other
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle.cpu_bench import CpuBaseline, cpu_model

@@ -14,6 +14,7 @@ try:  # pragma: no cover - depends on whether gelsim is installed
         GelsimError,
         InvalidQuery,
         LutResolutionMismatch,
+        ResolutionTooFine,
     )
 except Exception:  # noqa: BLE001
     class GelsimError(Exception):
@@ -28,4 +29,7 @@ except Exception:  # noqa: BLE001
     class LutResolutionMismatch(GelsimError):
         """Look-up table was calibrated for a different image size (errors.py:41-42)."""
 
-__all__ = ["GelsimError", "InvalidQuery", "DimensionMismatch", "LutResolutionMismatch"]
+    class ResolutionTooFine(GelsimError):
+        """Requested tactile grid is finer than the surface mesh resolves (errors.py:33-34)."""
+
+__all__ = ["GelsimError", "InvalidQuery", "DimensionMismatch", "LutResolutionMismatch", "ResolutionTooFine"]

@@ -77,16 +77,45 @@ class TactilePointGrid:
 
 def sample_tactile_points(sensor, rows: int, cols: int) -> TactilePointGrid:
     """Taxel [r, c] at x = linspace(-ax/2, ax/2, cols)[c], y = linspace(-ay/2,
-    ay/2, rows)[r], z = 0 on a flat pad (points.py:33-57)."""
+    ay/2, rows)[r] (points.py:33-57): at the pad's height on a flat pad; on a
+    curved gel dropped onto the surface mesh along -z from z = 1, with the
+    nearest face's outward normal (points.py:59-80), after the reference's
+    ResolutionTooFine check (points.py:40-45)."""
+    from .errors import ResolutionTooFine
+    from .sensors import ray_triangles_t
+
     ax, ay = sensor.active_area
     dx = ax / (cols - 1) if cols > 1 else ax
     dy = ay / (rows - 1) if rows > 1 else ay
+    mesh = sensor.surface_mesh
+    flat = sensor.is_flat()
+    if not flat:
+        feature = float(mesh.edge_lengths().min())
+        if min(dx, dy) < feature / 4.0:
+            raise ResolutionTooFine(f"grid spacing {min(dx, dy):.2e} under mesh feature {feature:.2e}/4")
     xs = np.linspace(-ax / 2, ax / 2, cols)
     ys = np.linspace(-ay / 2, ay / 2, rows)
     gx, gy = np.meshgrid(xs, ys, indexing="xy")
-    pts = np.stack([gx, gy, np.zeros_like(gx)], axis=-1)
-    normals = np.zeros_like(pts)
-    normals[..., 2] = 1.0
+    if flat:
+        z0 = float(mesh.vertices[0, 2])
+        pts = np.stack([gx, gy, np.full_like(gx, z0)], axis=-1)
+        normals = np.zeros_like(pts)
+        normals[..., 2] = 1.0
+        return TactilePointGrid(points=pts, rest_normals=normals, spacing=(dx, dy))
+    origins = np.stack([gx, gy, np.full_like(gx, 1.0)], axis=-1).reshape(-1, 3)
+    dirs = np.tile(np.array([0.0, 0.0, -1.0]), (len(origins), 1))
+    t = ray_triangles_t(origins, dirs, mesh.triangles)
+    if not np.all(np.isfinite(t)):
+        raise ValueError("active area extends beyond the surface mesh")
+    pts = (origins + dirs * t[:, None]).reshape(rows, cols, 3)
+    # nearest-face normal, outward = +z hemisphere (points.py:70-78)
+    tri = mesh.triangles
+    centroids = tri.mean(axis=1)
+    fn = mesh.face_normals()
+    flat_pts = pts.reshape(-1, 3)
+    d2 = ((flat_pts[:, None] - centroids[None]) ** 2).sum(-1)
+    n = fn[np.argmin(d2, axis=1)]
+    normals = (n * np.sign(n[:, 2:3])).reshape(rows, cols, 3)
     return TactilePointGrid(points=pts, rest_normals=normals, spacing=(dx, dy))
 
 

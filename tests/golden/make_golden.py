@@ -354,7 +354,24 @@ def make_extras(grid):
         raised = False
     except InvalidQuery:
         raised = True
-    np.savez_compressed(HERE / "extras.npz", cam_quat=quat, cam_pos=cam.pos, cam_f=np.array([cam.fx, cam.fy]),
+    # curved gel: the reference test's dome mesh (test_tactile_field.py:68-79)
+    from gelsim.geometry.mesh import TriMesh
+    from gelsim.tactile import sample_tactile_points as ref_points
+    n_d, rad, ext = 24, 0.05, 0.016
+    gxs = np.linspace(-ext, ext, n_d)
+    gx, gy = np.meshgrid(gxs, gxs, indexing="xy")
+    gz = np.sqrt(rad ** 2 - gx ** 2 - gy ** 2) - rad
+    dverts = np.stack([gx, gy, gz], axis=-1).reshape(-1, 3)
+    dfaces = np.array([[r * n_d + c, r * n_d + c + 1, r * n_d + c + n_d] for r in range(n_d - 1)
+                       for c in range(n_d - 1)] + [[r * n_d + c + 1, r * n_d + c + n_d + 1, r * n_d + c + n_d]
+                                                   for r in range(n_d - 1) for c in range(n_d - 1)])
+    dome = TriMesh(dverts, dfaces)
+    curved = TactileSensorSpec(active_area=(0.02, 0.02), surface_mesh=dome, image_size=(80, 60))
+    cgrid = ref_points(curved, 12, 12)
+    curved_bg = reference_depth(camera_for_sensor(curved), curved)
+    np.savez_compressed(HERE / "extras.npz", dome_vertices=dverts, dome_faces=dfaces,
+                        curved_points=cgrid.points, curved_normals=cgrid.rest_normals, curved_background=curved_bg,
+                        cam_quat=quat, cam_pos=cam.pos, cam_f=np.array([cam.fx, cam.fy]),
                         cam_c=np.array([cam.cx, cam.cy]), rays=rays, background=bg, points=inside, x_dot=x_dot,
                         rate=rate, x1=x1, rate1=rate1, mixed=mixed, mixed_raises=np.array(raised))
 

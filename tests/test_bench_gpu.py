@@ -40,12 +40,16 @@ def test_bench_json_contract():
     assert d["parity"]["ok"] and d["parity"]["rgb_max_lsb"] <= 1 and d["parity"]["mask_mismatches"] == 0
     assert len(d["validation"]["sha256"]) == 64 and d["validation"]["frames"] == 8192
     assert d["value_sustained"] > 0 and d["sustained"]["seconds"] >= 0.15
+    oc = d["other_configs"]  # configs 4 and 5, briefly, with their parity blocks
+    assert set(oc) == {"4", "5"}
+    for k, o in oc.items():
+        assert o["value"] > 0 and o["parity"]["ok"] and 0 < o["kernel_frac_of_hbm_peak"] < 1.05, k
 
 
 def test_bench_configs_run():
     for cfg in ("1", "4"):
         d = run_bench("--config", cfg, "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
-                      "--settle", "0")
+                      "--settle", "0", "--also", "")
         assert d["value"] > 0 and d["e2e"] is None
 
 
@@ -65,7 +69,7 @@ def test_bench_two_ranks_match_one_rank():
     green and the whole-job digest equals the N=1 run's."""
     import os
     common = ["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--settle", "0",
-              "--sustain-s", "0", "--envs", "512"]
+              "--sustain-s", "0", "--envs", "512", "--also", ""]
     one = run_bench(*common)
     env = dict(os.environ, TACSL_DIST_BACKEND="gloo")
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",

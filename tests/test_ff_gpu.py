@@ -361,3 +361,23 @@ def test_relative_penetration_rate_golden_and_invalid_query(golden, golden_grid)
     assert bool(z["mixed_raises"])
     with pytest.raises(InvalidQuery):
         relative_penetration_rate(query_sdf(golden_grid, z["mixed"]), z["x_dot"][:11])
+
+
+def test_force_field_on_curved_pad_taxels_vs_oracle(golden):
+    """Taxels of a curved gel (any point set) through K2 vs the oracle."""
+    from paper_2408_06506_b200.sensors import SurfaceMesh, TactileSensorSpec
+    z = golden("extras")
+    sensor = TactileSensorSpec(active_area=(0.02, 0.02), surface_mesh=SurfaceMesh(z["dome_vertices"],
+                                                                                   z["dome_faces"]))
+    pts = tactile.sample_tactile_points(sensor, 12, 12)
+    sdf = synthetic.peg_grid((32, 32, 64))
+    E = 64
+    obj, sen = synthetic.peg_states(E, 1, config_id=21)
+    o, s = obj, sen[:, 0]
+    fld = tactile.compute_force_field(pts, sdf, o[:, 0:3], o[:, 3:7], o[:, 7:10], o[:, 10:13], s[:, 0:3],
+                                      s[:, 3:7], s[:, 7:10], s[:, 10:13], tactile.PenaltyParams())
+    r_fn, r_ft, _ = O.compute_force_field(pts.points, *sdf_tuple(sdf), o[:, 0:3], o[:, 3:7], o[:, 7:10],
+                                          o[:, 10:13], s[:, 0:3], s[:, 3:7], s[:, 7:10], s[:, 10:13],
+                                          1000.0, 100.0, 10.0, 2.0)
+    assert vec_close(fld.f_n, r_fn, 1e-9, atol=1e-12)[0] and vec_close(fld.f_t, r_ft, 1e-9, atol=1e-12)[0]
+    assert (np.abs(r_fn).sum(-1) > 0).any()

@@ -146,3 +146,40 @@ def test_camera_validation_and_identity_quat():
     gu, gv = np.meshgrid(u, v, indexing="xy")
     d = np.stack([gu, gv, np.ones_like(gu)], axis=-1)
     np.testing.assert_array_equal(cam.rays(), d / np.linalg.norm(d, axis=-1, keepdims=True))
+
+
+def _dome(golden):
+    from paper_2408_06506_b200.sensors import SurfaceMesh, TactileSensorSpec
+    z = golden("extras")
+    mesh = SurfaceMesh(z["dome_vertices"], z["dome_faces"])
+    return z, TactileSensorSpec(active_area=(0.02, 0.02), surface_mesh=mesh, image_size=(80, 60))
+
+
+def test_curved_pad_taxels_normals_and_background_bit_exact(golden):
+    """Curved gel (sensors.py:32,39-50; points.py:59-80; camera.py:56-66):
+    taxels dropped onto the surface mesh, their nearest-face normals and the
+    membrane depth equal the reference's bit for bit (the reference test's
+    dome mesh, tests/test_tactile_field.py:68-79)."""
+    from paper_2408_06506_b200.sensors import camera_for_sensor, reference_depth
+    from paper_2408_06506_b200.tactile import sample_tactile_points
+    z, sensor = _dome(golden)
+    assert not sensor.is_flat()
+    g = sample_tactile_points(sensor, 12, 12)
+    np.testing.assert_array_equal(g.points, z["curved_points"])
+    np.testing.assert_array_equal(g.rest_normals, z["curved_normals"])
+    np.testing.assert_array_equal(reference_depth(camera_for_sensor(sensor), sensor), z["curved_background"])
+
+
+def test_curved_pad_errors(golden):
+    import pytest
+    from paper_2408_06506_b200.errors import ResolutionTooFine
+    from paper_2408_06506_b200.sensors import TactileSensorSpec
+    from paper_2408_06506_b200.tactile import sample_tactile_points
+    z, sensor = _dome(golden)
+    with pytest.raises(ResolutionTooFine):  # points.py:40-45
+        sample_tactile_points(sensor, 200, 200)
+    wide = TactileSensorSpec(active_area=(0.04, 0.04), surface_mesh=sensor.surface_mesh)
+    with pytest.raises(ValueError):  # points.py:63-64
+        sample_tactile_points(wide, 8, 8)
+    flat = TactileSensorSpec()
+    assert flat.is_flat() and sample_tactile_points(flat, 3, 4).points[..., 2].max() == 0.0

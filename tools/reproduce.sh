@@ -13,6 +13,8 @@ python tools/pcie_bw.py > "$out/pcie.json"
 python tools/bench_depth.py > "$out/depth.json"
 python tools/bench_augment.py > "$out/augment.txt"
 python tools/bench_pyramid.py 2048 > "$out/pyramid.txt"
+python tools/bench_pyramid_fused.py 8192 > "$out/pyramid_fused.txt"
+python tools/dropin_breakdown.py 1024 > "$out/dropin.txt"
 for d in 2 3 4; do python tools/bench_binned.py 8192 "$d"; done > "$out/binned.txt"
 python tools/bench_env.py 4096 > "$out/env.txt"
 python tools/k1_drift.py 40 > "$out/k1_drift.txt"

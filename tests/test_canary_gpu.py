@@ -112,3 +112,18 @@ def test_k3_k4_canaries(size, E):
     augment_device(rgb, cfg, seeds, seeds, tactile_rep="concat", nominal=np.float32([0.3, 0.4, 0.5]), out=out)
     torch.cuda.synchronize()
     assert intact(f64, torch.float64) and intact(f32, torch.float32) and intact(fo, torch.float32)
+
+
+@pytest.mark.parametrize("hw", [(480, 640), (36, 44), (8, 8), (484, 644), (12, 1024)])
+@pytest.mark.parametrize("n", [1, 5])
+def test_k7_canaries(hw, n):
+    """K7 writes every level's RGB (3 outputs per image) and nothing beyond."""
+    H, W = hw
+    _, cam, bg, lut, _ = synthetic.sensor_setup((W, H))
+    d = torch.rand((n, H, W), device="cuda") * 1e-3 + 0.02
+    views = [guarded((n, H >> lvl, W >> lvl, 3), torch.uint8) for lvl in range(3)]
+    smoothing.rgb_pyramid_fused_device(d, lut, levels=3, sigma=1.0, outs=[v for v, _ in views])
+    torch.cuda.synchronize()
+    for v, full in views:
+        assert intact(full, torch.uint8)
+        assert int(v.float().sum()) > 0

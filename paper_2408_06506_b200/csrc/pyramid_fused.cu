@@ -157,6 +157,9 @@ __global__ void __maxnreg__(128)
   const int H1 = H >> 1, H2 = H >> 2, W1 = W >> 1, W2 = W >> 2;
   const int WP = W + 2 * kPad, W1P = W1 + 2 * kPad, W2P = W2 + 2 * kPad;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // full[h]: half h of the tick's input rows landed
+  uint64_t* barA = full + 2;  // split barriers of the step loop (count: consumer warps)
+  uint64_t* barC = full + 3;
+  const int lane = threadIdx.x & 31;
   float* in_buf = reinterpret_cast<float*>(smem + 128);
   const int stage_f = kHalf * WP;
   float* s0 = in_buf + 2 * stage_f;
@@ -191,6 +194,8 @@ __global__ void __maxnreg__(128)
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
+    mbar_init(barA, cons_warps);
+    mbar_init(barC, cons_warps);
     fence_mbar_init();
     fence_proxy_async_smem();
     if (blockIdx.x < n) issue_tick(blockIdx.x, 0);
@@ -212,13 +217,66 @@ __global__ void __maxnreg__(128)
   acc1[0] = acc1[1] = f2(0.f, 0.f);
   acc2[0] = acc2[1] = 0.f;
   uint32_t ph = 0;  // phase of both half stages (each completes once per G tick)
+  uint32_t phA = 0, phC = 0;  // split barriers A (S0 rows of a step written) and C (S2 rows written)
   const int W3 = 3 * W, W13 = 3 * W1, W23 = 3 * W2;
+  // L2 of one (image, tick): runs one step late, in the gap of the next
+  // step's split barrier (see the loop below)
+  auto level2 = [&](int64_t im, int k) {
+    uint8_t* out2 = A.out[2] + (size_t)im * H2 * W23 + 3 * t;
+    // --------------------------------------------------------- L2 ---
+    if (k >= 1) {
+      const int sb = 2 * k - 6;
+      float wc[3];
+      float wl = 0.f, wr = 0.f;
+      uint8_t* orow = out2 + (sb + 1) * W23;
+      const float mx = (t == 0 || t == NQ - 1) ? 2.f : 1.f;
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        const int sr = sb + m;
+        const int r = min(max(sr, 0), H2 - 1);
+        const float* rp = s2 + (r & (RG::S2 - 1)) * W2P + kPad + t;
+        const float c = rp[0];
+        wc[0] = wc[1];
+        wc[1] = wc[2];
+        wc[2] = c;
+        if (m >= 2) {
+          const int y = sr - 1;
+          float hy = wc[2] - wc[0];
+          if (y == 0 || y == H2 - 1) hy = hy + hy;
+          const float hx = (wr - wl) * mx;
+          float v0, v1, v2;
+          shade<DEG>(A.L[2], hx, hy, v0, v1, v2);
+          if (act && y >= 0 && y < H2 && (m < 4 || y == H2 - 1)) {
+            orow[0] = (uint8_t)(q8(v0) & 0xFFu);
+            orow[1] = (uint8_t)(q8(v1) & 0xFFu);
+            orow[2] = (uint8_t)(q8(v2) & 0xFFu);
+          }
+          orow += W23;
+        }
+        wl = rp[-1];
+        wr = rp[1];
+      }
+    }
+  };
 
-  for (int64_t img = blockIdx.x; img < n; img += gridDim.x) {
+  // One step = one tick k of one image:
+  //   G(k)  -> arrive A -> [wait C(k-1), L2 of the previous step] -> wait A
+  //   -> (thread 0: next tick's TMA) -> L0(k) -> barrier B -> L1(k) -> arrive C
+  // A and C are mbarriers (arrive now, wait later): the wait for the slowest
+  // warp's G is filled with the previous step's L2, and the wait for its L1
+  // with this step's G, so only B blocks.  Hazards: S0 is rewritten by G
+  // only after B (all L0 reads done); S1 by L0 only after A (all L1 reads
+  // done: every warp arrives at A after its L1); S2 by L1 only after B (all
+  // L2 reads done before A).  Without a level 2 (LEVELS < 3) A and B are
+  // plain barriers.
+  int64_t img = blockIdx.x;
+  int k = 0;
+  int64_t pimg = -1;  // the step whose L2 is pending
+  int pk = 0;
+  while (img < n) {
     uint8_t* out0 = A.out[0] + (size_t)img * H * W3 + 3 * x0;
     uint8_t* out1 = LEVELS >= 2 ? A.out[1] + (size_t)img * H1 * W13 + 6 * t : nullptr;
-    uint8_t* out2 = LEVELS >= 3 ? A.out[2] + (size_t)img * H2 * W23 + 3 * t : nullptr;
-    for (int k = 0; k < K; ++k) {
+    {
       // ------------------------------------------------------------ G ---
       if (k <= kG) {
 #pragma unroll
@@ -294,12 +352,25 @@ __global__ void __maxnreg__(128)
         }
         ph ^= 1u;
       }
-      pyr_bar(n_cons);  // S0 rows of this tick are visible; the input stages are free
-      if (threadIdx.x == 0) {
-        if (k < kG) issue_tick(img, k + 1);
-        else if (k == kG && img + gridDim.x < n) issue_tick(img + gridDim.x, 0);
+    }
+    if constexpr (LEVELS >= 3) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(barA);
+      if (pimg >= 0) {
+        mbar_wait_parity(barC, phC);
+        phC ^= 1u;
+        if (pk >= 1) level2(pimg, pk);
       }
-
+      mbar_wait_parity(barA, phA);
+      phA ^= 1u;
+    } else {
+      pyr_bar(n_cons);  // S0 rows of this tick are visible; the input stages are free
+    }
+    if (threadIdx.x == 0) {
+      if (k < kG) issue_tick(img, k + 1);
+      else if (k == kG && img + gridDim.x < n) issue_tick(img + gridDim.x, 0);
+    }
+    {
       // ----------------------------------------------------------- L0 ---
       if (k >= 1) {
         const int sb = 8 * k - 10;
@@ -358,8 +429,9 @@ __global__ void __maxnreg__(128)
           }
         }
       }
-      pyr_bar(n_cons);  // S1 rows of this tick are visible; S0 reads done
-
+    }
+    pyr_bar(n_cons);  // B: S1 rows of this tick are visible; S0 reads done
+    {
       // ----------------------------------------------------------- L1 ---
       if constexpr (LEVELS >= 2) {
         if (k >= 1) {
@@ -416,43 +488,22 @@ __global__ void __maxnreg__(128)
           }
         }
       }
-      if constexpr (LEVELS >= 3) {
-        pyr_bar(n_cons);  // S2 rows of this tick are visible
-        // --------------------------------------------------------- L2 ---
-        if (k >= 1) {
-          const int sb = 2 * k - 6;
-          float wc[3];
-          float wl = 0.f, wr = 0.f;
-          uint8_t* orow = out2 + (sb + 1) * W23;
-          const float mx = (t == 0 || t == NQ - 1) ? 2.f : 1.f;
-#pragma unroll
-          for (int m = 0; m < 5; ++m) {
-            const int sr = sb + m;
-            const int r = min(max(sr, 0), H2 - 1);
-            const float* rp = s2 + (r & (RG::S2 - 1)) * W2P + kPad + t;
-            const float c = rp[0];
-            wc[0] = wc[1];
-            wc[1] = wc[2];
-            wc[2] = c;
-            if (m >= 2) {
-              const int y = sr - 1;
-              float hy = wc[2] - wc[0];
-              if (y == 0 || y == H2 - 1) hy = hy + hy;
-              const float hx = (wr - wl) * mx;
-              float v0, v1, v2;
-              shade<DEG>(A.L[2], hx, hy, v0, v1, v2);
-              if (act && y >= 0 && y < H2 && (m < 4 || y == H2 - 1)) {
-                orow[0] = (uint8_t)(q8(v0) & 0xFFu);
-                orow[1] = (uint8_t)(q8(v1) & 0xFFu);
-                orow[2] = (uint8_t)(q8(v2) & 0xFFu);
-              }
-              orow += W23;
-            }
-            wl = rp[-1];
-            wr = rp[1];
-          }
-        }
-      }
+    }
+    if constexpr (LEVELS >= 3) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(barC);
+      pimg = img;
+      pk = k;
+    }
+    if (++k == K) {
+      k = 0;
+      img += gridDim.x;
+    }
+  }
+  if constexpr (LEVELS >= 3) {
+    if (pimg >= 0) {  // the last step's L2
+      mbar_wait_parity(barC, phC);
+      if (pk >= 1) level2(pimg, pk);
     }
   }
 }

@@ -26,3 +26,8 @@ for f in sorted(out.glob("bench_c*.json")) + [out / "bench_ref.json"]:
     r = d.get("roofline") or {}
     print(f.name, round(d["value"]), d.get("ms_per_step"), r.get("frac"), (d.get("e2e") or {}).get("value"))
 PY
+# two ranks sharing the one GPU (gloo collectives): a functional check of the
+# sharding and the validation gather -- the digest must equal bench_c3.json's
+TACSL_DIST_BACKEND=gloo python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port 29517 bench.py --gpus 2 --steps 10 --no-cpu-baseline --no-e2e --also "" --sustain-s 0 \
+  > "$out/bench_c3_2ranks_gloo_1gpu.json"

@@ -215,6 +215,7 @@ def depth_to_rgb(depth, lut, out_dtype=None):
 
 
 _HOST_CHUNK_BYTES = 48 << 20  # input bytes per pipelined chunk of the numpy path
+_SMALL_CALL_BYTES = 4 << 20   # below this the numpy path is one upload / launch / download
 
 
 def _depth_to_rgb_host(values, lut, want_u8, dev):
@@ -230,6 +231,17 @@ def _depth_to_rgb_host(values, lut, want_u8, dev):
     n = int(np.prod(lead, dtype=np.int64)) if lead else 1
     src = np.ascontiguousarray(values.reshape(n, H, W),
                                dtype=np.float64 if src_dtype == t.float64 else np.float32)
+    if src.nbytes <= _SMALL_CALL_BYTES:
+        # a per-finger / per-env call: latency over bandwidth -- no staging
+        # pipeline, no side streams
+        v = _device.as_f32(src, dev)
+        if want_u8:
+            u8 = t.empty((n, H, W, 3), dtype=t.uint8, device=dev)
+            depth_to_rgb_device(v, lut, out_u8=u8)
+            return _device.download(u8).reshape(lead + (H, W, 3))
+        f32 = t.empty((n, H, W, 3), dtype=t.float32, device=dev)
+        depth_to_rgb_device(v, lut, out_f32=f32)
+        return _device.download(_device.widen_f64(f32)).reshape(lead + (H, W, 3))
     out_dtype = t.uint8 if want_u8 else t.float64
     pin_out = _device.pinned_empty((n, H, W, 3), out_dtype)
     dl = device_lut(lut)

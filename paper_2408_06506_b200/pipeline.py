@@ -405,13 +405,3 @@ def frame_digests(outputs):
         names.append(name)
         cols.append(out)
     return names, t.stack(cols, dim=1) if cols else None
-
-
-def frame_checksum(rgb_u8, f_n, f_t) -> np.ndarray:
-    """Cheap per-shard digest for cross-rank validation: (sum of RGB bytes,
-    sum |f_n|, sum |f_t|) as float64."""
-    t = _device.torch()
-    parts = [x.sum(dtype=t.float64) if x is not None and k == 0 else
-             (x.abs().sum(dtype=t.float64) if x is not None else t.zeros((), dtype=t.float64))
-             for k, x in enumerate((rgb_u8, f_n, f_t))]
-    return t.stack([p.to(parts[0].device) for p in parts])

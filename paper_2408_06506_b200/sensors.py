@@ -133,15 +133,6 @@ def camera_for_sensor(sensor: TactileSensorSpec) -> TactileCamera:
                          width=W, height=H, near=sensor.near, far=sensor.far)
 
 
-def flat_pad_triangles(active_area, skirt: float = 0.002) -> np.ndarray:
-    """The flat pad's gel surface: two triangles at z = 0 covering the active
-    area plus a skirt, (2, 3, 3) (sensors.py:17-23 flat_pad_mesh)."""
-    hx = active_area[0] / 2.0 + skirt
-    hy = active_area[1] / 2.0 + skirt
-    v = np.array([[-hx, -hy, 0.0], [hx, -hy, 0.0], [hx, hy, 0.0], [-hx, hy, 0.0]])
-    return v[np.array([[0, 1, 2], [0, 2, 3]])]
-
-
 def _cross(a, b):
     """np.cross component order: each product rounded, then subtracted."""
     return np.stack([a[..., 1] * b[..., 2] - a[..., 2] * b[..., 1],

@@ -314,7 +314,8 @@ TACSL_API int tacsl_sensor_step(tacsl_lut_t lut, const float* depth, int64_t n_i
  * tacsl_separable_filter and tacsl_depth_to_rgb level by level, with only
  * the depth read and the RGB written to memory.  Requires
  * tacsl_rgb_pyramid_supported(height, width, radius, levels) (levels 1-3,
- * radius 0-4, width % 4 == 0 and <= 1024, height % 4 == 0) else
+ * radius 0-4, width % 4 == 0 (% 8 with 3 levels) and <= 1024, height % 4
+ * == 0) else
  * INVALID_ARGUMENT; LUT size mismatch -> LUT_RESOLUTION_MISMATCH. */
 TACSL_API int tacsl_rgb_pyramid_supported(int height, int width, int radius, int levels);
 TACSL_API int tacsl_rgb_pyramid(const tacsl_lut_t* luts, int levels, const float* depth, int64_t n_images,

@@ -222,40 +222,32 @@ __global__ void __maxnreg__(128)
   // L2 of one (image, tick): runs one step late, in the gap of the next
   // step's split barrier (see the loop below)
   auto level2 = [&](int64_t im, int k) {
-    uint8_t* out2 = A.out[2] + (size_t)im * H2 * W23 + 3 * t;
-    // --------------------------------------------------------- L2 ---
-    if (k >= 1) {
-      const int sb = 2 * k - 6;
-      float wc[3];
-      float wl = 0.f, wr = 0.f;
-      uint8_t* orow = out2 + (sb + 1) * W23;
-      const float mx = (t == 0 || t == NQ - 1) ? 2.f : 1.f;
+    // level 2 by (row, pixel pair): the tick's two level-2 rows split over
+    // two groups of W/8 threads, every warp equally busy (the phase's time
+    // is its busiest warp's); K1's pair arithmetic
+    const int NP2 = W2 >> 1;
+    const int g = (int)threadIdx.x / NP2;
+    const int p = (int)threadIdx.x - g * NP2;
+    if (k < 1 || g > 1) return;
+    const float n0 = p == 0 ? 2.f : 1.f, n1 = p == NP2 - 1 ? 2.f : 1.f;
 #pragma unroll
-      for (int m = 0; m < 5; ++m) {
-        const int sr = sb + m;
-        const int r = min(max(sr, 0), H2 - 1);
-        const float* rp = s2 + (r & (RG::S2 - 1)) * W2P + kPad + t;
-        const float c = rp[0];
-        wc[0] = wc[1];
-        wc[1] = wc[2];
-        wc[2] = c;
-        if (m >= 2) {
-          const int y = sr - 1;
-          float hy = wc[2] - wc[0];
-          if (y == 0 || y == H2 - 1) hy = hy + hy;
-          const float hx = (wr - wl) * mx;
-          float v0, v1, v2;
-          shade<DEG>(A.L[2], hx, hy, v0, v1, v2);
-          if (act && y >= 0 && y < H2 && (m < 4 || y == H2 - 1)) {
-            orow[0] = (uint8_t)(q8(v0) & 0xFFu);
-            orow[1] = (uint8_t)(q8(v1) & 0xFFu);
-            orow[2] = (uint8_t)(q8(v2) & 0xFFu);
-          }
-          orow += W23;
-        }
-        wl = rp[-1];
-        wr = rp[1];
-      }
+    for (int e = 0; e < 2; ++e) {
+      // e = 0: row 2k-5+g (the tick's regular rows); e = 1: row 2k-3 when it
+      // is the image's last level-2 row (its down neighbour is itself)
+      const int y = 2 * k - 5 + g + 2 * e;
+      const bool valid = e == 0 ? (y >= 0 && y < H2) : (g == 0 && y == H2 - 1);
+      if (!valid) continue;
+      const int ru = max(y - 1, 0), rd = min(y + 1, H2 - 1);
+      const float* rc = s2 + (y & (RG::S2 - 1)) * W2P + kPad + 2 * p;
+      const float2 up = *reinterpret_cast<const float2*>(s2 + (ru & (RG::S2 - 1)) * W2P + kPad + 2 * p);
+      const float2 dn = *reinterpret_cast<const float2*>(s2 + (rd & (RG::S2 - 1)) * W2P + kPad + 2 * p);
+      const float2 c = *reinterpret_cast<const float2*>(rc);
+      uint32_t h0, h1, h2;
+      shade_pair<DEG>(A.L[2], up, c, rc[-1], rc[2], dn, y == 0 || y == H2 - 1, n0, n1, h0, h1, h2);
+      uint16_t* o = reinterpret_cast<uint16_t*>(A.out[2] + ((size_t)im * H2 + y) * W23 + 6 * p);
+      o[0] = (uint16_t)h0;
+      o[1] = (uint16_t)h1;
+      o[2] = (uint16_t)h2;
     }
   };
 
@@ -569,7 +561,7 @@ using namespace tacsl;
 
 extern "C" int tacsl_rgb_pyramid_supported(int height, int width, int radius, int levels) {
   if (levels < 1 || levels > 3 || radius < 0 || radius > 4) return 0;
-  if (width < 8 || width % 4 != 0 || width / 4 > kPMaxCons) return 0;
+  if (width < 8 || width % (levels >= 3 ? 8 : 4) != 0 || width / 4 > kPMaxCons) return 0;
   if (height < 4 || height % 4 != 0) return 0;
   return pyramid_smem(radius, width) <= 227 * 1024 ? 1 : 0;
 }
@@ -581,8 +573,8 @@ extern "C" int tacsl_rgb_pyramid(const tacsl_lut_t* luts, int levels, const floa
   if (n_images < 0) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb_pyramid: negative image count");
   if (!tacsl_rgb_pyramid_supported(height, width, radius, levels))
     return set_error(TACSL_ERR_INVALID_ARGUMENT,
-                     "rgb_pyramid: needs levels in [1,3], radius in [0,4], width % 4 == 0 (8..1024), "
-                     "height % 4 == 0 (see tacsl_rgb_pyramid_supported)");
+                     "rgb_pyramid: needs levels in [1,3], radius in [0,4], width % 4 == 0 (% 8 for 3 "
+                     "levels; 8..1024), height % 4 == 0 (see tacsl_rgb_pyramid_supported)");
   if (!luts || !out || (radius > 0 && !taps)) return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb_pyramid: null pointer");
   const int deg = luts[0] ? luts[0]->degree : 0;
   for (int l = 0; l < levels; ++l) {
@@ -594,8 +586,9 @@ extern "C" int tacsl_rgb_pyramid(const tacsl_lut_t* luts, int levels, const floa
   if (n_images == 0) return TACSL_OK;
   if (!depth || (reinterpret_cast<uintptr_t>(depth) & 15) != 0)
     return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb_pyramid: depth must be 16-byte aligned");
-  if ((reinterpret_cast<uintptr_t>(out[0]) & 3) != 0 || (levels >= 2 && (reinterpret_cast<uintptr_t>(out[1]) & 1)))
-    return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb_pyramid: output alignment (4 B level 0, 2 B level 1)");
+  if ((reinterpret_cast<uintptr_t>(out[0]) & 3) != 0 || (levels >= 2 && (reinterpret_cast<uintptr_t>(out[1]) & 1)) ||
+      (levels >= 3 && (reinterpret_cast<uintptr_t>(out[2]) & 1)))
+    return set_error(TACSL_ERR_INVALID_ARGUMENT, "rgb_pyramid: output alignment (4 B level 0, 2 B levels 1-2)");
   PyrArgs A;
   std::memset(&A, 0, sizeof(A));
   const int K = 2 * radius + 1;

@@ -114,7 +114,7 @@ def test_k3_k4_canaries(size, E):
     assert intact(f64, torch.float64) and intact(f32, torch.float32) and intact(fo, torch.float32)
 
 
-@pytest.mark.parametrize("hw", [(480, 640), (36, 44), (8, 8), (484, 644), (12, 1024)])
+@pytest.mark.parametrize("hw", [(480, 640), (36, 48), (8, 8), (484, 648), (12, 1024)])
 @pytest.mark.parametrize("n", [1, 5])
 def test_k7_canaries(hw, n):
     """K7 writes every level's RGB (3 outputs per image) and nothing beyond."""

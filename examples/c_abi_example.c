@@ -1,8 +1,10 @@
-/* The C ABI without Python: flat-depth RGB and a static press force field
- * through libtacsl_b200.so, checked against closed-form answers
- * (render/lut.py:52-54: flat depth -> the LUT's background colour;
- * tactile/field.py:61-76: a taxel pressed d = -1 mm into a plane with
- * k_n = 1000 N/m feels |f_n| = 1 N).
+/* The C ABI without Python: flat-depth RGB (one level, and the smoothed
+ * three-level pyramid of K7), a static press force field and the
+ * InvalidQuery status through libtacsl_b200.so, checked against closed-form
+ * answers (render/lut.py:52-54: flat depth -> the LUT's background colour at
+ * every level; tactile/field.py:61-76: a taxel pressed d = -1 mm into a
+ * plane with k_n = 1000 N/m feels |f_n| = 1 N; geometry/sdf.py:324-328:
+ * an out-of-grid query -> InvalidQuery).
  *
  *   gcc -O2 -I include -I /usr/local/cuda/include examples/c_abi_example.c \
  *       -L paper_2408_06506_b200 -ltacsl_b200 -L /usr/local/cuda/lib64 -lcudart \
@@ -60,6 +62,34 @@ int main(void) {
     return 1;
   }
 
+  /* ---- K7: sigma = 1 smoothing + a 3-level RGB pyramid of the same flat
+   * maps: every level is the background colour too */
+  tacsl_lut_t luts[3];
+  unsigned char* d_lvl[3];
+  int bad_pyr = 0;
+  for (int l = 0; l < 3; ++l) {
+    CHECK(tacsl_lut_create(coeffs, 2, W >> l, H >> l, &luts[l]));
+    cudaMalloc((void**)&d_lvl[l], (size_t)N * (H >> l) * (W >> l) * 3);
+  }
+  const float taps[9] = {0.00013383f, 0.00443305f, 0.05399100f, 0.24197072f, 0.39894353f,
+                         0.24197072f, 0.05399100f, 0.00443305f, 0.00013383f};
+  if (!tacsl_rgb_pyramid_supported(H, W, 4, 3)) {
+    fprintf(stderr, "pyramid shape not supported\n");
+    return 1;
+  }
+  CHECK(tacsl_rgb_pyramid(luts, 3, d_depth, N, H, W, taps, 4, d_lvl, NULL));
+  for (int l = 0; l < 3; ++l) {
+    const size_t np = (size_t)N * (H >> l) * (W >> l);
+    unsigned char* h = (unsigned char*)malloc(np * 3);
+    cudaMemcpy(h, d_lvl[l], np * 3, cudaMemcpyDeviceToHost);
+    for (size_t i = 0; i < np; ++i)
+      for (int c = 0; c < 3; ++c) bad_pyr += h[3 * i + c] != (unsigned char)lrint(bg[c] * 255.0);
+    free(h);
+    cudaFree(d_lvl[l]);
+    tacsl_lut_destroy(luts[l]);
+  }
+  printf("pyramid: %d channel values differ from the background colour over 3 levels\n", bad_pyr);
+
   /* ---- force field: a plane z <= 0 as an SDF (d = z, grad = +z), one taxel
    * at the sensor origin, sensor 1 mm below the surface, at rest */
   const int n = 8;
@@ -99,7 +129,28 @@ int main(void) {
   cudaMemcpy(fn, d_fn, sizeof fn, cudaMemcpyDeviceToHost);
   cudaMemcpy(wr, d_w, sizeof wr, cudaMemcpyDeviceToHost);
   printf("force field: f_n = (%.6f, %.6f, %.6f) N, wrench force z = %.6f N\n", fn[0], fn[1], fn[2], wr[2]);
-  const int ok = bad == 0 && fabs(fn[2] - 1.0) < 1e-9 && fabs(wr[2] - 1.0) < 1e-9;
+  /* ---- relative_penetration_rate: one query outside the grid -> InvalidQuery */
+  const double nrm[6] = {0, 0, 1, 0, 0, 1}, xd[3] = {0, 0, -0.01};
+  const unsigned char valid[2] = {1, 0};
+  double *d_n, *d_x, *d_rate;
+  unsigned char* d_valid;
+  int* d_flag;
+  cudaMalloc((void**)&d_n, sizeof nrm);
+  cudaMalloc((void**)&d_x, sizeof xd);
+  cudaMalloc((void**)&d_rate, 2 * sizeof(double));
+  cudaMalloc((void**)&d_valid, 2);
+  cudaMalloc((void**)&d_flag, sizeof(int));
+  cudaMemcpy(d_n, nrm, sizeof nrm, cudaMemcpyHostToDevice);
+  cudaMemcpy(d_x, xd, sizeof xd, cudaMemcpyHostToDevice);
+  cudaMemcpy(d_valid, valid, 2, cudaMemcpyHostToDevice);
+  const int rc_bad = tacsl_relative_penetration_rate(d_n, d_valid, d_x, 2, 1, d_rate, d_flag, NULL);
+  const int rc_ok = tacsl_relative_penetration_rate(d_n, d_valid, d_x, 1, 1, d_rate, d_flag, NULL);
+  double rate;
+  cudaMemcpy(&rate, d_rate, sizeof rate, cudaMemcpyDeviceToHost);
+  printf("penetration rate: status %d for an out-of-grid query (INVALID_QUERY = %d), d_dot = %.3f\n", rc_bad,
+         TACSL_ERR_INVALID_QUERY, rate);
+  const int ok = bad == 0 && bad_pyr == 0 && fabs(fn[2] - 1.0) < 1e-9 && fabs(wr[2] - 1.0) < 1e-9 &&
+                 rc_bad == TACSL_ERR_INVALID_QUERY && rc_ok == TACSL_OK && fabs(rate + 0.01) < 1e-15;
   tacsl_lut_destroy(lut);
   tacsl_sdf_destroy(sdf);
   printf(ok ? "ok\n" : "FAILED\n");

@@ -1,7 +1,8 @@
 """The C ABI from C: examples/c_abi_example.c is compiled with gcc against
 include/tacsl_b200.h and libtacsl_b200.so (no Python in the loop) and checks
-closed-form answers (flat depth -> background colour; a 1 mm press on a
-plane -> |f_n| = 1 N; the resolution-mismatch status code)."""
+closed-form answers (flat depth -> background colour, also at every level
+of the K7 pyramid; a 1 mm press on a plane -> |f_n| = 1 N; the
+resolution-mismatch and invalid-query status codes)."""
 import shutil
 import subprocess
 from pathlib import Path
@@ -25,3 +26,4 @@ def test_c_abi_example(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.strip().endswith("ok"), out.stdout
     assert "0 of" in out.stdout
+    assert "pyramid: 0 channel values differ" in out.stdout

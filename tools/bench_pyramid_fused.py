@@ -1,7 +1,7 @@
 """Time K7 (the one-pass smoothing + 3-level RGB pyramid) against the
 unfused chain on N 480x640 depth maps (config 5: N = 8192).
 
-    python tools/bench_pyramid_fused.py [N] [--stages S]
+    python tools/bench_pyramid_fused.py [N]
 """
 import os
 import sys
@@ -48,4 +48,4 @@ for name, fn in (("K7 fused", fused), ("unfused chain", chain)):
     ms = sorted(per)[1]
     print(f"{name}: {ms:.3f} ms for {N} frames {W}x{H} (3 levels, sigma=1): "
           f"{alg / ms / 1e6:.0f} GB/s algorithmic = {alg / ms / 1e6 / peak:.3f} of {peak} GB/s "
-          f"(stages={os.environ.get('TACSL_PYR_STAGES', '3')})")
+          "")

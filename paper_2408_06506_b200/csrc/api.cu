@@ -1,4 +1,5 @@
 // C-ABI plumbing: error state, device checks, LUT/SDF handles, to_uint8.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -119,6 +120,51 @@ int tacsl_lut_create(const double* coeffs, int degree, int width, int height, ta
 
 void tacsl_lut_destroy(tacsl_lut_t lut) { delete lut; }
 
+}  // extern "C"
+
+namespace {
+// float32 quad grid + per-axis Lipschitz bounds for the force field's
+// certified contact-mask pre-pass (handles.h).  Best effort: without it the
+// force field runs its fp64 kernel.
+void build_quads(tacsl_sdf_s* h, const double* v, const int32_t dims[3]) {
+  h->quads = nullptr;
+  h->lip[0] = h->lip[1] = h->lip[2] = 0.0f;
+  const int64_t nx = dims[0], ny = dims[1], nz = dims[2];
+  const int64_t n = nx * ny * nz;
+  double lip[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = 0; i < n; ++i)
+    if (!(std::fabs(v[i]) < 1e30)) return;  // non-finite / beyond float range
+  std::vector<float4> q((size_t)n);
+  for (int64_t x = 0; x < nx; ++x)
+    for (int64_t y = 0; y < ny; ++y)
+      for (int64_t z = 0; z < nz; ++z) {
+        const int64_t c = (x * ny + y) * nz + z;
+        const int64_t y1 = std::min(y + 1, ny - 1), z1 = std::min(z + 1, nz - 1);
+        q[(size_t)c] = make_float4((float)v[c], (float)v[(x * ny + y) * nz + z1], (float)v[(x * ny + y1) * nz + z],
+                                   (float)v[(x * ny + y1) * nz + z1]);
+        if (x + 1 < nx) lip[0] = std::max(lip[0], std::fabs(v[c + ny * nz] - v[c]));
+        if (y + 1 < ny) lip[1] = std::max(lip[1], std::fabs(v[c + nz] - v[c]));
+        if (z + 1 < nz) lip[2] = std::max(lip[2], std::fabs(v[c + 1] - v[c]));
+      }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  float4* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, (size_t)n * sizeof(float4));
+  if (e == cudaSuccess) e = cudaMemcpy(d, q.data(), (size_t)n * sizeof(float4), cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    if (d) cudaFree(d);
+    cudaGetLastError();
+    return;
+  }
+  h->quads = d;
+  for (int a = 0; a < 3; ++a) h->lip[a] = (float)(lip[a] * (1.0 + 1e-6)) + 1e-30f;  // rounded up
+}
+}  // namespace
+
+extern "C" {
+
 int tacsl_sdf_create(int device, const double* values, const double* gradients, const int32_t dims[3],
                      const double origin[3], double spacing, tacsl_sdf_t* out) {
   if (!out || !values || !gradients || !dims || !origin)
@@ -153,6 +199,7 @@ int tacsl_sdf_create(int device, const double* values, const double* gradients, 
   h->device = device;
   h->grid = dptr;
   h->values = vptr;
+  build_quads(h, values, dims);
   for (int a = 0; a < 3; ++a) {
     h->dims[a] = dims[a];
     h->origin[a] = origin[a];
@@ -169,6 +216,7 @@ void tacsl_sdf_destroy(tacsl_sdf_t sdf) {
   cudaSetDevice(sdf->device);
   cudaFree(sdf->grid);
   cudaFree(sdf->values);
+  if (sdf->quads) cudaFree(sdf->quads);
   cudaSetDevice(prev);
   delete sdf;
 }

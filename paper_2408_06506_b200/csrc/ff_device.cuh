@@ -47,6 +47,8 @@ struct Grid {
   const double* __restrict__ values;  // d only, compact (8 B per cell): the mask path's gathers
   int nx, ny, nz;
   double ox, oy, oz, spacing, inv_spacing;
+  const float4* __restrict__ quads;  // fp32 corner quads (handles.h), or null
+  float lsum;                        // sum of the per-axis Lipschitz bounds (m per cell)
 };
 
 // 256-bit read-only load (LDG.E.ENL2.256 on sm_100): one trilinear corner
@@ -118,30 +120,49 @@ __device__ __forceinline__ double interp_d(const Grid& g, const Cell& c) {
   return add_rn(mul_rn(d0, c.uz), mul_rn(d1, c.wz));
 }
 
-// Trilinear gradient, renormalised: n = g / max(|g|, 1e-12) (sdf.py:314-316)
-__device__ __forceinline__ V3 interp_n(const Grid& g, const Cell& c) {
+// Trilinear gradient, renormalised: n = g / max(|g|, 1e-12) (sdf.py:314-316).
+// With d_out, also the distance from the same corner loads, in
+// interp_d_fast's lerp form (bit-identical to it: the cells' d is values).
+// The eight {d, gx, gy, gz} corners of a cell, corner k = 4 dx + 2 dy + dz.
+__device__ __forceinline__ void load_corners(const Grid& g, int base, double4 cv[8]) {
+  const int sy = g.nz, sx = g.ny * g.nz;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cv[k] = ldg256(g.cells + base + ((k >> 2) & 1) * sx + ((k >> 1) & 1) * sy + (k & 1));
+}
+
+// interp_n on corners already loaded (load_corners); see interp_n
+__device__ __forceinline__ V3 interp_n_from(const double4 cv[8], const Cell& c, double* d_out) {
   double gx = 0.0, gy = 0.0, gz = 0.0;
-  double ax[2], ay[2], az[2];
+  double ax[2], ay[2], az[2], ad[2];
 #pragma unroll
   for (int dz = 0; dz < 2; ++dz) {
-    double bx[2], by[2], bz[2];
+    double bx[2], by[2], bz[2], bd[2];
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
-      const double4 lo = ldg256(g.cells + corner(g, c, 2 * dy + dz));
-      const double4 hi = ldg256(g.cells + corner(g, c, 4 + 2 * dy + dz));
+      const double4 lo = cv[2 * dy + dz];
+      const double4 hi = cv[4 + 2 * dy + dz];
+      bd[dy] = fma(c.wx, hi.x - lo.x, lo.x);
       bx[dy] = lo.y * c.ux + hi.y * c.wx;
       by[dy] = lo.z * c.ux + hi.z * c.wx;
       bz[dy] = lo.w * c.ux + hi.w * c.wx;
     }
+    ad[dz] = fma(c.wy, bd[1] - bd[0], bd[0]);
     ax[dz] = bx[0] * c.uy + bx[1] * c.wy;
     ay[dz] = by[0] * c.uy + by[1] * c.wy;
     az[dz] = bz[0] * c.uy + bz[1] * c.wy;
   }
+  if (d_out) *d_out = fma(c.wz, ad[1] - ad[0], ad[0]);
   gx = ax[0] * c.uz + ax[1] * c.wz;
   gy = ay[0] * c.uz + ay[1] * c.wz;
   gz = az[0] * c.uz + az[1] * c.wz;
   const double inv = rsqrt(fmax(gx * gx + gy * gy + gz * gz, 1e-24));
   return v3(gx * inv, gy * inv, gz * inv);
+}
+
+__device__ __forceinline__ V3 interp_n(const Grid& g, const Cell& c, double* d_out = nullptr) {
+  double4 cv[8];
+  load_corners(g, c.base, cv);
+  return interp_n_from(cv, c, d_out);
 }
 
 struct Query {
@@ -228,6 +249,7 @@ struct FFArgs {
   uint8_t* __restrict__ contact;
   float* __restrict__ obs;
   unsigned long long* counter;  // dynamic frame dispatch (fused step), zeroed before the launch
+  const float4* __restrict__ taxf;  // taxels as {x, y, z, |x|+|y|+|z|} fp32 (force_field_quad_kernel)
 };
 
 // Taxels first, first+stride, ... of one sensor frame (tactile/field.py:
@@ -378,6 +400,16 @@ struct FrameC {
   double Ms[9], sp[3];  // p_w = Ms p + sp (sensor pose)
   double Mo[9], op[3];  // n_w = Mo n; object position
   double sv[3], sw[3], ov[3], ow[3];
+  // fp32 pre-pass (force_field_quad_kernel): rel ~ A32 p + b32, and the
+  // per-frame constants of its certified error bounds
+  float A32[9], b32[3];
+  float amax, bmax;  // max |A_ik|, max |b_i| (rounded up)
+  float kt, k0;      // distance bound tau(p) = kt * (amax |p|_1 + bmax) + k0
+  // contact path in the sensor frame (unit quaternions): n_s = Mso n,
+  // x_dot_s = kv + om x p  (Mso = Ms^T Mo, kv = Ms^T (s_v - o_v) - w_o,s x c_s,
+  // om = Ms^T (s_w - o_w), c_s = Ms^T (s_pos - o_pos))
+  double Mso[9], kv[3], om[3];
+  int unit;  // both quaternions unit to 1e-12 (else the world-frame path)
 };
 
 // row-major matrix of quat_rotate(q, .) (transforms.py:36-41)
@@ -396,11 +428,60 @@ __device__ __forceinline__ void quat_matrix(double w, V3 q, double* M) {
   M[8] = 1.0 - 2.0 * (xx + yy);
 }
 
+// The quad kernel's extra per-frame constants (force_field.cu): the fp32
+// fold, the bounds of its certified error (max |A|, max |b|) and the
+// sensor-frame contact path's Ms^T Mo, kv, om.  val = this lane's A / b entry.
+template <typename OutT>
+__device__ __forceinline__ void frame_setup_quad(const FFArgs<OutT>& A, FrameC& C, int lane, double val,
+                                                 const State& S, const State& O, const double* Ms,
+                                                 const double* Mo) {
+  const Grid& g = A.grid;
+  // max |A|, max |b|
+  // (NaN poses propagate: fmax drops NaN, so test them explicitly)
+  double am = lane < 9 ? fabs(val) : 0.0, bm = (lane >= 9 && lane < 12) ? fabs(val) : 0.0;
+  bool bad = val != val;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
+    bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 15) {
+    const float inf = __int_as_float(0x7f800000);
+    C.amax = bad ? inf : __double2float_ru(am);
+    C.bmax = bad ? inf : __double2float_ru(bm);
+    constexpr float u = 5.9604645e-8f;  // 2^-24
+    C.kt = __fmul_ru(8.0f * u, g.lsum);
+    C.k0 = __fmul_ru(g.lsum, 1e-7f + 8.0f * u);
+  }
+  if (lane == 16) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) C.Mso[3 * i + j] = Ms[i] * Mo[j] + Ms[3 + i] * Mo[3 + j] + Ms[6 + i] * Mo[6 + j];
+    const double qs = S.qw * S.qw + S.qv.x * S.qv.x + S.qv.y * S.qv.y + S.qv.z * S.qv.z;
+    const double qo = O.qw * O.qw + O.qv.x * O.qv.x + O.qv.y * O.qv.y + O.qv.z * O.qv.z;
+    C.unit = fabs(qs - 1.0) < 1e-12 && fabs(qo - 1.0) < 1e-12;
+  } else if (lane == 17) {
+    // Ms^T a for a world vector a
+    auto to_s = [&](V3 a) {
+      return v3(Ms[0] * a.x + Ms[3] * a.y + Ms[6] * a.z, Ms[1] * a.x + Ms[4] * a.y + Ms[7] * a.z,
+                Ms[2] * a.x + Ms[5] * a.y + Ms[8] * a.z);
+    };
+    const V3 vs = to_s(v3(S.v.x - O.v.x, S.v.y - O.v.y, S.v.z - O.v.z));
+    const V3 ws = to_s(S.w), wo = to_s(O.w);
+    const V3 cs = to_s(v3(S.pos.x - O.pos.x, S.pos.y - O.pos.y, S.pos.z - O.pos.z));
+    const V3 wc = cross(wo, cs);
+    C.kv[0] = vs.x - wc.x, C.kv[1] = vs.y - wc.y, C.kv[2] = vs.z - wc.z;
+    C.om[0] = ws.x - wo.x, C.om[1] = ws.y - wo.y, C.om[2] = ws.z - wo.z;
+  }
+}
+
 // Per-frame constants, built by one warp: every lane forms both rotation
 // matrices (a few dozen flops on broadcast loads) and writes its share of
 // the 48 entries (A, b on lanes 0-11), so the CTA waits for one short
 // dependency chain only.
-template <typename OutT>
+template <bool QUAD = false, typename OutT>
 __device__ __forceinline__ void frame_setup_warp(const FFArgs<OutT>& A, int64_t frame, FrameC& C, int lane) {
   const int64_t e = frame / A.n_sensors;
   const int s = (int)(frame - e * A.n_sensors);
@@ -410,15 +491,22 @@ __device__ __forceinline__ void frame_setup_warp(const FFArgs<OutT>& A, int64_t 
   quat_matrix(S.qw, S.qv, Ms);
   quat_matrix(O.qw, O.qv, Mo);
   const Grid& g = A.grid;
+  double val = 0.0;
   if (lane < 9) {  // A = (Mo^T Ms) / h
     const int i = lane / 3, j = lane % 3;
-    C.A[lane] = (Mo[i] * Ms[j] + Mo[3 + i] * Ms[3 + j] + Mo[6 + i] * Ms[6 + j]) * g.inv_spacing;
+    val = (Mo[i] * Ms[j] + Mo[3 + i] * Ms[3 + j] + Mo[6 + i] * Ms[6 + j]) * g.inv_spacing;
+    C.A[lane] = val;
+    if (QUAD) C.A32[lane] = (float)val;
   } else if (lane < 12) {  // b = (Mo^T (s_pos - o_pos) - origin) / h
     const int i = lane - 9;
     const double org = i == 0 ? g.ox : (i == 1 ? g.oy : g.oz);
-    C.b[i] = ((Mo[i] * (S.pos.x - O.pos.x) + Mo[3 + i] * (S.pos.y - O.pos.y) + Mo[6 + i] * (S.pos.z - O.pos.z)) -
-              org) * g.inv_spacing;
-  } else if (lane == 12) {
+    val = ((Mo[i] * (S.pos.x - O.pos.x) + Mo[3 + i] * (S.pos.y - O.pos.y) + Mo[6 + i] * (S.pos.z - O.pos.z)) -
+           org) * g.inv_spacing;
+    C.b[i] = val;
+    if (QUAD) C.b32[i] = (float)val;
+  }
+  if (QUAD) frame_setup_quad(A, C, lane, val, S, O, Ms, Mo);
+  if (lane == 12) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) C.Ms[k] = Ms[k];
     C.sp[0] = S.pos.x, C.sp[1] = S.pos.y, C.sp[2] = S.pos.z;
@@ -474,6 +562,8 @@ inline Grid make_grid(tacsl_sdf_t sdf) {
   g.oz = sdf->origin[2];
   g.spacing = sdf->spacing;
   g.inv_spacing = 1.0 / sdf->spacing;  // correctly rounded (IEEE division on the host)
+  g.quads = sdf->quads;
+  g.lsum = sdf->lip[0] + sdf->lip[1] + sdf->lip[2];
   return g;
 }
 

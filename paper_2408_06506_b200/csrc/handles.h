@@ -36,6 +36,13 @@ struct tacsl_sdf_s {
   int device;
   double4* grid;   // (nx, ny, nz) {d, gx, gy, gz}, z fastest, 32 B per cell (force field)
   double* values;  // (nx, ny, nz) d only, 8 B per cell (sphere tracing)
+  // The force field's contact-mask pre-pass (force_field.cu, quad kernel):
+  // per cell (x, y, z) the float32 values {v(x,y,z), v(x,y,z+1), v(x,y+1,z),
+  // v(x,y+1,z+1)} (indices clamped at the far faces), 16 B per cell, so the
+  // eight trilinear corners are two 128-bit gathers; null when the grid has
+  // non-finite or out-of-float-range values (the fp64 kernel runs instead).
+  float4* quads;
+  float lip[3];  // max |v(i+1) - v(i)| along each axis (rounded up): Lipschitz bounds of the interpolant
   int dims[3];
   double origin[3];
   double spacing;

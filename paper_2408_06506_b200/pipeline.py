@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _device, smoothing
+from . import _device, smoothing, tactile
 from .geometry import device_sdf
 from .render import depth_to_rgb_device, device_lut
 from .tactile import device_taxels, force_field_device
@@ -78,7 +78,8 @@ class SensorArray:
         rgb_launches = (1 + int(self.sigma > 0) + 2 * (self.levels - 1)) if self.with_rgb else 0
         if self.fused_pyramid:
             rgb_launches = 1
-        self.launches_per_step = 1 if self.fused else rgb_launches + int(with_ff)
+        ff_launches = tactile.force_field_launches(self.rows, self.cols) if with_ff else 0
+        self.launches_per_step = 1 if self.fused else rgb_launches + ff_launches
         self._workspace = t.zeros(1, dtype=t.int64, device=dev) if self.fused else None
         self._ff_stream = t.cuda.Stream(device=dev) if overlap else None
         self._graph = None

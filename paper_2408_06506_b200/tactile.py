@@ -148,6 +148,18 @@ def device_taxels(points, device):
     return tens
 
 
+def force_field_launches(rows: int, cols: int) -> int:
+    """Kernels one force-field call launches without kinematics: the taxels'
+    fp32 copy and the certified fp32-mask kernel on dense pads (more than
+    1024 taxels, rows*cols % 4 == 0; csrc/force_field.cu, quad kernel), else
+    the fp64 fast kernel alone.  TACSL_FF_QUAD=0/1 forces the choice."""
+    import os
+    n = rows * cols
+    q = os.environ.get("TACSL_FF_QUAD")
+    want = (q == "1") if q is not None else n > 1024
+    return 2 if want and n % 4 == 0 else 1
+
+
 def _state_array(pos, quat, v, w, E, name):
     """Broadcast pos (3), quat (4), linvel (3), angvel (3) to an (E, 13) state."""
     parts = []

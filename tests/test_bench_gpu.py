@@ -28,7 +28,7 @@ def test_bench_json_contract():
                    ("gpu_launches", int), ("clocks", dict)):
         assert isinstance(d[k], typ), k
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3 and d["vs_baseline"] is None
-    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] == 2 * 5
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] == 2 * 5  # K1, K2 (20x25 pads: the fp64 kernel)
     assert "workload" in d["config"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0

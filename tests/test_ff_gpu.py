@@ -257,13 +257,16 @@ def test_query_sdf_sentinel_and_device_tensors():
     assert torch.equal(qd.distance.cpu(), torch.from_numpy(q.distance))
 
 
+@pytest.mark.parametrize("kernel", ["quad", "fp64"])
 @pytest.mark.parametrize("offset", [0.0, 100.0])
-def test_fast_mask_chain_equals_exact_chain(monkeypatch, offset):
+def test_fast_mask_chain_equals_exact_chain(monkeypatch, offset, kernel):
     """force_field_fast_kernel (affine cell coordinates + exact fallback near
     every decision boundary) against the all-exact kernel and the oracle:
     identical contact masks, forces within 1e-9 relative -- also with the
-    envs placed 100 m from the world origin."""
+    envs placed 100 m from the world origin.  ``quad`` is the certified fp32
+    pre-pass (force_field_quad_kernel), ``fp64`` the fp64 fast kernel."""
     t = torch
+    monkeypatch.setenv("TACSL_FF_QUAD", "1" if kernel == "quad" else "0")
     sdf = synthetic.peg_grid((32, 32, 64))
     pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 20, 25)
     E, S = 256, 2
@@ -305,10 +308,12 @@ def test_fast_mask_chain_equals_exact_chain(monkeypatch, offset):
     assert vec_close(fast[1].reshape(rt.shape), rt, FF_RTOL, atol=1e-9)[0]
 
 
-def test_fast_chain_decides_boundary_taxels_exactly(monkeypatch):
+@pytest.mark.parametrize("kernel", ["quad", "fp64"])
+def test_fast_chain_decides_boundary_taxels_exactly(monkeypatch, kernel):
     """Taxels placed exactly on the contact surface (d = 0 in the grid) and
     on the grid boundary go through the exact fallback: masks still match."""
     t = torch
+    monkeypatch.setenv("TACSL_FF_QUAD", "1" if kernel == "quad" else "0")
     sdf = geometry.box_grid((0.1, 0.1, 0.02), dims=(48, 48, 24), padding=0.01)
     pts = sensor_grid(12, 12)
     E = 64
@@ -381,3 +386,104 @@ def test_force_field_on_curved_pad_taxels_vs_oracle(golden):
                                           1000.0, 100.0, 10.0, 2.0)
     assert vec_close(fld.f_n, r_fn, 1e-9, atol=1e-12)[0] and vec_close(fld.f_t, r_ft, 1e-9, atol=1e-12)[0]
     assert (np.abs(r_fn).sum(-1) > 0).any()
+
+
+# ------------------------------------- certified fp32 pre-pass (quad kernel) --
+
+def _ff_run(sdf, pts_dev, rows, cols, obj, sen, S=1, fp64=True):
+    t = torch
+    E = obj.shape[0]
+    dev = t.device("cuda")
+    dt = t.float64 if fp64 else t.float32
+    f_n = t.empty((E, S, rows, cols, 3), dtype=dt, device=dev)
+    f_t = t.empty_like(f_n)
+    w = t.empty((E, S, 6), dtype=t.float64, device=dev)
+    c = t.empty((E, S, rows, cols), dtype=t.uint8, device=dev)
+    tactile.force_field_device(sdf, pts_dev, rows, cols, t.from_numpy(obj).to(dev),
+                               t.from_numpy(np.ascontiguousarray(sen)).to(dev), PenaltyParams(), f_n, f_t,
+                               wrench=w, contact=c, n_sensors=S)
+    t.cuda.synchronize()
+    return [x.cpu().numpy() for x in (f_n, f_t, w, c)]
+
+
+def _ff_vs_exact(monkeypatch, sdf, pts_dev, rows, cols, obj, sen, S=1):
+    monkeypatch.setenv("TACSL_FF_QUAD", "1")  # the quad kernel also on these small pads
+    quad = _ff_run(sdf, pts_dev, rows, cols, obj, sen, S)
+    monkeypatch.setenv("TACSL_FF_EXACT", "1")
+    exact = _ff_run(sdf, pts_dev, rows, cols, obj, sen, S)
+    monkeypatch.delenv("TACSL_FF_EXACT")
+    assert np.array_equal(quad[3], exact[3])
+    for a, b in zip(quad[:3], exact[:3]):
+        assert vec_close(a, b, 1e-9, atol=1e-12)[0]
+    return quad
+
+
+def test_quad_kernel_taxels_on_grid_faces_and_lines(monkeypatch, plate_sdf):
+    """Taxels exactly on the SDF grid's faces, on cell boundaries, just
+    inside / outside the one-cell shell and far outside: the fp32
+    classification and its explicit shell test decide validity exactly."""
+    g = plate_sdf
+    h, o, up = g.spacing, g.origin, g.upper
+    xs = np.concatenate([o[0] + h * np.array([-3.0, -1.0, -0.5, 0.0, 1e-12, 0.5, 1.0, 2.0, 7.0]),
+                         up[0] - h * np.array([2.0, 1.0, 0.5, 0.0, -1e-12, -0.5, -1.0, -3.0])])
+    ys = np.concatenate([o[1] + h * np.array([-1.0, 0.0, 0.25, 1.0]), up[1] - h * np.array([1.0, 0.0, -0.25, -1.0]),
+                         [0.0, 0.003, -0.004, 0.011]])
+    rows, cols = len(ys), len(xs)                         # 12 x 17 = 204 taxels (a multiple of 4)
+    zs = [up[2], g.origin[2], 0.01, 0.0099999, 0.0100001]  # grid top, bottom, box top (d = 0) and around it
+    E = len(zs) * 4
+    pts = np.zeros((rows, cols, 3))
+    pts[..., 0] = xs[None, :]
+    pts[..., 1] = ys[:, None]
+    obj = np.zeros((E, 13))
+    obj[:, 3] = 1.0
+    sen = np.zeros((E, 1, 13))
+    sen[:, 0, 3] = 1.0
+    rng = np.random.default_rng(3)
+    for e in range(E):
+        sen[e, 0, 2] = zs[e // 4]
+        sen[e, 0, 7:10] = rng.normal(0, 0.01, 3)
+    dev = torch.device("cuda")
+    tax = torch.from_numpy(pts.reshape(-1, 3)).to(dev)
+    quad = _ff_vs_exact(monkeypatch, g, tax, rows, cols, obj, sen)
+    assert 0 < quad[3].mean() < 1
+    objE, senE = obj, sen.reshape(E, 13)
+    rn, rt, rk = O.compute_force_field(pts, *sdf_tuple(g), objE[:, 0:3], objE[:, 3:7], objE[:, 7:10], objE[:, 10:13],
+                                       senE[:, 0:3], senE[:, 3:7], senE[:, 7:10], senE[:, 10:13])
+    assert np.array_equal(quad[3].reshape(E, rows, cols).astype(bool), rk["d"] < 0)
+
+
+def test_quad_kernel_nan_and_non_unit_poses(monkeypatch):
+    """A NaN object pose (the reference: every taxel invalid, zero forces)
+    and non-unit quaternions (the world-frame contact path)."""
+    sdf = synthetic.peg_grid((32, 32, 64))
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 20, 25)
+    obj, sen = synthetic.peg_states(16, 1, config_id=31)
+    obj[3, 0] = np.nan
+    obj[5, 3:7] *= 1.25
+    sen[7, 0, 3:7] *= 0.8
+    tax = tactile.device_taxels(pts, torch.device("cuda"))
+    quad = _ff_vs_exact(monkeypatch, sdf, tax, 20, 25, obj, sen)
+    assert not quad[3][3].any() and np.all(quad[0][3] == 0)
+
+
+def test_quad_kernel_fallbacks_and_taxel_refresh(monkeypatch, plate_sdf):
+    """rows*cols % 4 != 0 and an SDF with non-finite values run the fp64
+    kernel; a taxel tensor edited in place is never served stale."""
+    sdf = synthetic.peg_grid((32, 32, 64))
+    obj, sen = synthetic.peg_states(8, 1, config_id=32)
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 5, 5)  # 25 taxels
+    _ff_vs_exact(monkeypatch, sdf, tactile.device_taxels(pts, torch.device("cuda")), 5, 5, obj, sen)
+    inf_sdf = synthetic.peg_grid((32, 32, 64))
+    inf_sdf.values = inf_sdf.values.copy()
+    inf_sdf.values[0, 0, 0] = np.inf                     # far corner, never interpolated by the pad
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 20, 25)
+    tax = tactile.device_taxels(pts, torch.device("cuda")).clone()
+    _ff_vs_exact(monkeypatch, inf_sdf, tax, 20, 25, obj, sen)
+    monkeypatch.setenv("TACSL_FF_QUAD", "1")
+    first = _ff_run(sdf, tax, 20, 25, obj, sen)
+    tax[:, 2] += 0.0005                                   # same pointer, new contents
+    moved = _ff_run(sdf, tax, 20, 25, obj, sen)
+    fresh = _ff_run(sdf, tax.clone(), 20, 25, obj, sen)
+    for a, b in zip(moved, fresh):
+        assert np.array_equal(a, b)
+    assert not np.array_equal(first[3], moved[3])

@@ -213,3 +213,40 @@ def test_config4_shape_fast_kernel_vs_oracle():
                        n_sensors=1)
     torch.cuda.synchronize()
     assert torch.equal(sub_n, f_n[ti]) and torch.equal(sub_t, f_t[ti])
+
+
+def test_config4_quad_kernel_equals_fp64_kernel_full_batch(monkeypatch):
+    """The whole config-4 batch (16384 x 8000 taxels, 128^3 SDF): the
+    certified fp32 pre-pass (quad kernel, the default on dense pads) and the
+    fp64 fast kernel give identical contact masks on all 131 M taxels, and
+    forces / wrenches within the fp32 output rounding."""
+    from conftest import vec_close as vc
+    from paper_2408_06506_b200.sensors import TactileSensorSpec
+    from paper_2408_06506_b200.tactile import sample_tactile_points
+    sdf = synthetic.peg_grid((128, 128, 128))
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 80, 100)
+    E4 = 16384
+    obj, sen = synthetic.peg_states(E4, 1, config_id=4)
+    o = torch.from_numpy(obj).cuda()
+    s = torch.from_numpy(np.ascontiguousarray(sen)).cuda()
+    tax = device_taxels(pts, o.device)
+
+    def run():
+        f_n = torch.empty((E4, 1, 80, 100, 3), dtype=torch.float32, device="cuda")
+        f_t = torch.empty_like(f_n)
+        w = torch.empty((E4, 1, 6), dtype=torch.float64, device="cuda")
+        c = torch.empty((E4, 1, 80, 100), dtype=torch.uint8, device="cuda")
+        force_field_device(sdf, tax, 80, 100, o, s, PenaltyParams(), f_n, f_t, wrench=w, contact=c, n_sensors=1)
+        torch.cuda.synchronize()
+        return f_n, f_t, w, c
+
+    q = run()
+    monkeypatch.setenv("TACSL_FF_QUAD", "0")
+    f = run()
+    assert torch.equal(q[3], f[3])
+    assert 0.2 < q[3].float().mean().item() < 0.35
+    for a, b in zip(q[:2], f[:2]):
+        d = (a.double() - b.double()).norm(dim=-1)
+        assert bool((d <= 2e-7 * b.double().norm(dim=-1) + 1e-12).all())
+    scale = (q[0].double() + q[1].double()).abs().sum(dim=(1, 2, 3)).unsqueeze(-1)
+    assert bool(((q[2] - f[2])[..., 0:3].abs() <= 1e-6 * scale + 1e-12).all())

@@ -1,5 +1,6 @@
 """One K2 launch at config-4 shape (80x100 taxels, 128^3 peg SDF) on N frames
-(for ncu captures)."""
+(for ncu captures); a second argument "lifted" moves every peg 1.5 mm off
+its pad (no contact)."""
 import sys
 from pathlib import Path
 
@@ -15,6 +16,9 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 _, cam, bg, lut, pts = synthetic.sensor_setup((320, 240), (80, 100))
 sdf = device_sdf(synthetic.peg_grid((128, 128, 128)), torch.device("cuda", 0))
 obj, sen = synthetic.peg_states(N, 1, config_id=4)
+if len(sys.argv) > 2 and sys.argv[2] == "lifted":
+    from paper_2408_06506_b200.transforms import quat_rotate
+    obj[:, 0:3] += quat_rotate(sen[:, 0, 3:7], np.array([0.0, 0.0, 0.0015]))
 o = torch.from_numpy(obj).cuda()
 s = torch.from_numpy(np.ascontiguousarray(sen)).cuda()
 tax = device_taxels(pts, o.device)

@@ -464,7 +464,7 @@ def run_other_config(cid, dev, args, peak):
         with torch.cuda.graph(g):
             arr._launch_rgb(c.depth)
     else:
-        name, kbytes = "force_field_fast_kernel", bytes_["ff"]
+        name, kbytes = arr.ff_kernel_name(), bytes_["ff"]
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             arr._launch_ff(c.obj, c.sen)
@@ -753,9 +753,14 @@ def main():
         rule = ("SURVEY.md 8d: 4 B fp32 depth read per level-0 pixel + 3 B uint8 RGB written per pixel of "
                 "every pyramid level (intermediates are not algorithmic bytes)")
     else:
-        kname, kms, kbytes = "force_field_fast_kernel", k2_ms, bytes_["ff"]
-        desc = ("force_field_fast_kernel (K2 force field + wrench; float64 / L2-gather-latency bound, "
-                "HBM fraction shown)")
+        kname, kms, kbytes = arr.ff_kernel_name(), k2_ms, bytes_["ff"]
+        if kname == "force_field_quad_kernel":
+            desc = ("force_field_quad_kernel (K2 force field + wrench: certified fp32 contact-mask pass, fp64 "
+                    "contact path on a warp queue; timed with its taxel fp32-copy launch; issue-bound, HBM "
+                    "fraction shown)")
+        else:
+            desc = ("force_field_fast_kernel (K2 force field + wrench; float64 / L2-gather-latency bound, "
+                    "HBM fraction shown)")
         rule = "24 B/taxel fp32 f_n,f_t written + 208 B fp64 states read + 48 B wrench per frame"
     k_gbs = kbytes / (kms / 1e3) / 1e9
     traffic = traffic_from_profiles(f"{kname}/config{wl.config_id}/world{world}")

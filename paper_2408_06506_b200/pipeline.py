@@ -104,6 +104,11 @@ class SensorArray:
             ff = F * (taxel_out + 13 * 8 + 6 * 8) + self.E * 13 * 8
         return {"rgb": rgb, "ff": ff, "total": rgb + ff}
 
+    def ff_kernel_name(self) -> str:
+        """The K2 variant a step launches (csrc/force_field.cu)."""
+        return ("force_field_quad_kernel" if tactile.force_field_launches(self.rows, self.cols) == 2
+                else "force_field_fast_kernel")
+
     def image_kernel_name(self) -> str:
         return "pyramid_fused_kernel" if self.fused_pyramid else "image_pipeline"
 

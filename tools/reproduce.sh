@@ -18,6 +18,7 @@ python tools/dropin_breakdown.py 1024 > "$out/dropin.txt"
 for d in 2 3 4; do python tools/bench_binned.py 8192 "$d"; done > "$out/binned.txt"
 python tools/bench_env.py 4096 > "$out/env.txt"
 python tools/k1_drift.py 40 > "$out/k1_drift.txt"
+bash tools/ff_quad_ab.sh > "$out/ff_quad_ab.txt"
 python - "$out" <<'PY'
 import json, sys, pathlib
 out = pathlib.Path(sys.argv[1])

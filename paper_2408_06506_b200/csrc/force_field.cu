@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(MAXT, MINB) force_field_fast_kernel(const FFAr
 // Contact taxels then recompute the cell and d in float64 from the fast
 // fold (as force_field_fast_kernel does) for their forces; taxels the bound
 // cannot decide run the reference chain (exact_rel).  The taxels come from
-// an fp32 copy {x, y, z, |p|_1} (taxel_f32_kernel), four per lane at
+// a per-call fp32 copy {x, y, z, |p|_1} (taxel_f32_kernel), four per lane at
 // lane + 32 j of a warp's 128-taxel block: coalesced 16-B loads, issued one
 // block ahead, eight gathers in flight, and coalesced 16-B zero stores.
 constexpr float kU32 = 5.9604645e-8f;  // 2^-24
@@ -661,36 +661,33 @@ __global__ void __launch_bounds__(256) taxel_f32_kernel(const double* __restrict
   }
 }
 
-// One fp32 taxel buffer per (device, taxel array, count), kept for the
-// process (taxel sets are few and small); refreshed by every call, so an
-// array edited in place is never stale.  Null when it cannot be allocated
-// (e.g. first use under stream capture): the caller then runs the fp64 kernel.
-float4* taxel_buffer(int device, const double* taxels, int n, cudaStream_t stream) {
-  struct Entry {
-    int device;
-    const double* src;
-    int n;
-    float4* buf;
-  };
+// The fp32 taxel copy lives for one call: stream-ordered allocation from the
+// device's default memory pool (kept warm: release threshold raised once per
+// device), so nothing is cached across calls -- an array edited in place or
+// freed and reallocated is never stale -- and it is legal under stream
+// capture (allocation / free nodes in the graph).  Null on failure: the
+// caller then runs the fp64 kernel.
+float4* taxel_scratch(int device, int n, cudaStream_t stream) {
   static std::mutex mu;
-  static std::vector<Entry> cache;
-  std::lock_guard<std::mutex> lock(mu);
-  for (const Entry& e : cache)
-    if (e.device == device && e.src == taxels && e.n == n) return e.buf;
-  // no allocation under stream capture (it would invalidate the capture)
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+  static std::vector<int> warmed;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(warmed.begin(), warmed.end(), device) == warmed.end()) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaGetLastError();
+      warmed.push_back(device);
+    }
+  }
+  void* buf = nullptr;
+  if (cudaMallocAsync(&buf, (size_t)n * sizeof(float4), stream) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  if (cap != cudaStreamCaptureStatusNone) return nullptr;
-  float4* buf = nullptr;
-  if (cudaMalloc(&buf, (size_t)n * sizeof(float4)) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  cache.push_back(Entry{device, taxels, n, buf});
-  return buf;
+  return static_cast<float4*>(buf);
 }
 
 int check_params(const tacsl_penalty_t& p) {
@@ -781,12 +778,15 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
               al(obs, 16) && al(contact, 4);
   float4* taxf = nullptr;
   if (quad) {
-    taxf = taxel_buffer(current_device(), taxels, n_taxels, s);
+    taxf = taxel_scratch(current_device(), n_taxels, s);
     quad = taxf != nullptr;
   }
   if (quad) {
     taxel_f32_kernel<<<std::min(elementwise_blocks(n_taxels), 64u), 256, 0, s>>>(taxels, n_taxels, taxf);
-    if (int rc = check_launch("taxel_f32_kernel")) return rc;
+    if (int rc = check_launch("taxel_f32_kernel")) {
+      cudaFreeAsync(taxf, s);
+      return rc;
+    }
   }
   auto launch = [&](auto out_tag) {
     using O = decltype(out_tag);
@@ -818,7 +818,9 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
   };
   if (out_fp64) launch(double{});
   else launch(float{});
-  return check_launch("force_field_kernel");
+  const int launched = check_launch("force_field_kernel");
+  if (taxf) cudaFreeAsync(taxf, s);
+  return launched;
 }
 
 int tacsl_net_wrench(const double* f_n, const double* f_t, const double* points, int64_t frames, int rows, int cols,

@@ -774,7 +774,8 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
   // on 20x25 pads the fp64 fast kernel is faster (and overlaps K1 better)
   const char* qenv = std::getenv("TACSL_FF_QUAD");  // "0": never, "1": whenever eligible
   const bool want_quad = qenv ? qenv[0] == '1' : n_taxels > kQuadMinTaxels;
-  bool quad = want_quad && !kin && !exact && sdf->quads && n_taxels % 4 == 0 && al(f_n, 16) && al(f_t, 16) &&
+  bool quad = want_quad && !kin && !exact && sdf->quads && n_taxels % 4 == 0 && n_taxels < (1 << 29) &&
+              al(f_n, 16) && al(f_t, 16) &&
               al(obs, 16) && al(contact, 4);
   float4* taxf = nullptr;
   if (quad) {

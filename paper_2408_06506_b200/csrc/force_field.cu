@@ -417,6 +417,105 @@ __device__ __forceinline__ void drain_taxel(const FFArgs<OutT>& A, const FrameC&
 // warps' fp32 blocks overlap its latency (no CTA barrier until the wrench).
 constexpr int kWarpQueue = 160;  // < 32 left over + 128 appended per block
 
+// The certified fp32 decisions for one warp's block of 128 taxels (four per
+// lane, lane + 32 j; cnt a multiple of 4): per taxel two bits of the
+// result -- 0 no contact, 1 contact, 2 undecided (the reference chain) --
+// and the fp32 cell index in idx[j] (for a contact taxel).
+template <typename OutT>
+__device__ __forceinline__ unsigned classify_block(const FFArgs<OutT>& A, const FrameC& C, int blk, int cnt,
+                                                   const float4 tfs[4], int lane, int idx_out[4]) {
+  const Grid& g = A.grid;
+  const int mx = g.nx - 1, my = g.ny - 1, mz = g.nz - 1;  // rel in [0, m] is inside
+  const int nyz = g.ny * g.nz;
+  // the frame constants come from shared memory every block: the drain
+  // between blocks needs the registers
+  float a[9], b[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) a[k] = C.A32[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) b[k] = C.b32[k];
+  const float amax = C.amax, bmax = C.bmax, kt = C.kt, k0 = C.k0;
+  // cells [1, m-2] (rel in [1, m-1)) are inside and rel < -1 or >= m+1
+  // outside whenever mrel < 1 (sb < 1e6); NaN fails both: shell -> exact
+  const float hx = (float)(mx - 1), hy = (float)(my - 1), hz = (float)(mz - 1);
+  const float ox = (float)(mx + 1), oy = (float)(my + 1), oz = (float)(mz + 1);
+  const bool full = cnt == 128;
+  QuadTaxel t[4];
+  bool shell = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int k = lane + 32 * j;
+    const bool live = full || k < cnt;
+    const float4 tf = tfs[j];
+    const float x = tf.x, y = tf.y, z = tf.z;
+    const float rx = fmaf(a[0], x, fmaf(a[1], y, fmaf(a[2], z, b[0])));
+    const float ry = fmaf(a[3], x, fmaf(a[4], y, fmaf(a[5], z, b[1])));
+    const float rz = fmaf(a[6], x, fmaf(a[7], y, fmaf(a[8], z, b[2])));
+    const float sb = fmaf(amax, tf.w, bmax);
+    t[j].tau = fmaf(kt, sb, k0);
+    bool in, out;
+    int ix, iy, iz;
+    {
+    const bool ok = live & (sb < 1e6f);  // mrel < 1
+    in = ok & (rx >= 1.0f) & (rx < hx) & (ry >= 1.0f) & (ry < hy) & (rz >= 1.0f) & (rz < hz);
+    out = !live | (ok & ((rx < -1.0f) | (rx >= ox) | (ry < -1.0f) | (ry >= oy) | (rz < -1.0f) |
+                                    (rz >= oz)));
+    // floor by round-down onto 1.5 * 2^23 (exact for rel in [1, 2^22]; only used when inside)
+    const float tx = __fadd_rd(rx, kFloorMagic), ty = __fadd_rd(ry, kFloorMagic), tz = __fadd_rd(rz, kFloorMagic);
+    ix = __float_as_int(tx) - 0x4B400000, iy = __float_as_int(ty) - 0x4B400000,
+              iz = __float_as_int(tz) - 0x4B400000;
+    t[j].wx = rx - (tx - kFloorMagic);
+    t[j].wy = ry - (ty - kFloorMagic);
+    t[j].wz = rz - (tz - kFloorMagic);
+    }
+    t[j].cls = in ? 1 : (out ? 0 : 2);
+    t[j].idx = in ? (ix * g.ny + iy) * g.nz + iz : 0;
+    shell |= !(in | out);
+  }
+  if (shell) {  // the one-cell shell round the grid faces: explicit margins
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (t[j].cls != 2) continue;
+      const float4 tf = __ldg(A.taxf + blk + lane + 32 * j);
+      const float x = tf.x, y = tf.y, z = tf.z;
+      const float rx = fmaf(a[0], x, fmaf(a[1], y, fmaf(a[2], z, b[0])));
+      const float ry = fmaf(a[3], x, fmaf(a[4], y, fmaf(a[5], z, b[1])));
+      const float rz = fmaf(a[6], x, fmaf(a[7], y, fmaf(a[8], z, b[2])));
+      const float mrel = fmaf(8.0f * kU32, fmaf(amax, tf.w, bmax), 1e-7f);
+      bool in = true, out = false;
+      shell_axis(rx, mrel, mx, in, out);
+      shell_axis(ry, mrel, my, in, out);
+      shell_axis(rz, mrel, mz, in, out);
+      if (out) {
+        t[j].cls = 0;
+      } else if (in) {  // 0 < rel < m: floor lands in [0, m - 1]
+        const int ix = min((int)rx, mx - 1), iy = min((int)ry, my - 1), iz = min((int)rz, mz - 1);
+        t[j].wx = rx - (float)ix;
+        t[j].wy = ry - (float)iy;
+        t[j].wz = rz - (float)iz;
+        t[j].idx = (ix * g.ny + iy) * g.nz + iz;
+        t[j].cls = 1;
+      }
+    }
+  }
+  // per taxel, two bits: 0 no contact, 1 contact, 2 exact chain
+  unsigned kinds = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 lo = __ldg(g.quads + t[j].idx), hi = __ldg(g.quads + t[j].idx + nyz);
+    // x lerps of the (z, z+1) x (y, y+1) corner pairs, then y, then z
+    const float e00 = fmaf(t[j].wx, hi.x - lo.x, lo.x), e01 = fmaf(t[j].wx, hi.y - lo.y, lo.y);
+    const float e10 = fmaf(t[j].wx, hi.z - lo.z, lo.z), e11 = fmaf(t[j].wx, hi.w - lo.w, lo.w);
+    const float f0 = fmaf(t[j].wy, e10 - e00, e00), f1 = fmaf(t[j].wy, e11 - e01, e01);
+    const float d32 = fmaf(t[j].wz, f1 - f0, f0);
+    const bool clear = fabsf(d32) * (1.0f - 16.0f * kU32) > 2.0f * t[j].tau;
+    const unsigned kind = t[j].cls == 0 ? 0u : (t[j].cls == 1 && clear ? (d32 < 0.0f ? 1u : 0u) : 2u);
+    kinds |= kind << (2 * j);
+    idx_out[j] = t[j].idx;
+  }
+  return kinds;
+}
+
 template <typename OutT, int MINB, int MAXT>
 __global__ void __launch_bounds__(MAXT, MINB) force_field_quad_kernel(const FFArgs<OutT> A) {
   const int64_t frame = blockIdx.x;
@@ -455,93 +554,9 @@ __global__ void __launch_bounds__(MAXT, MINB) force_field_quad_kernel(const FFAr
 #pragma unroll
     for (int j = 0; j < 4; ++j) tfs[j] = tnext[j];
     if (blk + 128 * nwarps < A.n_taxels) load_block(blk + 128 * nwarps, tnext);
-    // the frame constants come from shared memory every block: the drain
-    // between blocks needs the registers
-    float a[9], b[3];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) a[k] = C.A32[k];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) b[k] = C.b32[k];
-    const float amax = C.amax, bmax = C.bmax, kt = C.kt, k0 = C.k0;
-    // cells [1, m-2] (rel in [1, m-1)) are inside and rel < -1 or >= m+1
-    // outside whenever mrel < 1 (sb < 1e6); NaN fails both: shell -> exact
-    const float hx = (float)(mx - 1), hy = (float)(my - 1), hz = (float)(mz - 1);
-    const float ox = (float)(mx + 1), oy = (float)(my + 1), oz = (float)(mz + 1);
+    int idx[4];
+    const unsigned kinds = classify_block(A, C, blk, cnt, tfs, lane, idx);
     const bool full = cnt == 128;
-    QuadTaxel t[4];
-    bool shell = false;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int k = lane + 32 * j;
-      const bool live = full || k < cnt;
-      const float4 tf = tfs[j];
-      const float x = tf.x, y = tf.y, z = tf.z;
-      const float rx = fmaf(a[0], x, fmaf(a[1], y, fmaf(a[2], z, b[0])));
-      const float ry = fmaf(a[3], x, fmaf(a[4], y, fmaf(a[5], z, b[1])));
-      const float rz = fmaf(a[6], x, fmaf(a[7], y, fmaf(a[8], z, b[2])));
-      const float sb = fmaf(amax, tf.w, bmax);
-      t[j].tau = fmaf(kt, sb, k0);
-      bool in, out;
-      int ix, iy, iz;
-      {
-      const bool ok = live & (sb < 1e6f);  // mrel < 1
-      in = ok & (rx >= 1.0f) & (rx < hx) & (ry >= 1.0f) & (ry < hy) & (rz >= 1.0f) & (rz < hz);
-      out = !live | (ok & ((rx < -1.0f) | (rx >= ox) | (ry < -1.0f) | (ry >= oy) | (rz < -1.0f) |
-                                      (rz >= oz)));
-      // floor by round-down onto 1.5 * 2^23 (exact for rel in [1, 2^22]; only used when inside)
-      const float tx = __fadd_rd(rx, kFloorMagic), ty = __fadd_rd(ry, kFloorMagic), tz = __fadd_rd(rz, kFloorMagic);
-      ix = __float_as_int(tx) - 0x4B400000, iy = __float_as_int(ty) - 0x4B400000,
-                iz = __float_as_int(tz) - 0x4B400000;
-      t[j].wx = rx - (tx - kFloorMagic);
-      t[j].wy = ry - (ty - kFloorMagic);
-      t[j].wz = rz - (tz - kFloorMagic);
-      }
-      t[j].cls = in ? 1 : (out ? 0 : 2);
-      t[j].idx = in ? (ix * g.ny + iy) * g.nz + iz : 0;
-      shell |= !(in | out);
-    }
-    if (shell) {  // the one-cell shell round the grid faces: explicit margins
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (t[j].cls != 2) continue;
-        const float4 tf = __ldg(A.taxf + blk + lane + 32 * j);
-        const float x = tf.x, y = tf.y, z = tf.z;
-        const float rx = fmaf(a[0], x, fmaf(a[1], y, fmaf(a[2], z, b[0])));
-        const float ry = fmaf(a[3], x, fmaf(a[4], y, fmaf(a[5], z, b[1])));
-        const float rz = fmaf(a[6], x, fmaf(a[7], y, fmaf(a[8], z, b[2])));
-        const float mrel = fmaf(8.0f * kU32, fmaf(amax, tf.w, bmax), 1e-7f);
-        bool in = true, out = false;
-        shell_axis(rx, mrel, mx, in, out);
-        shell_axis(ry, mrel, my, in, out);
-        shell_axis(rz, mrel, mz, in, out);
-        if (out) {
-          t[j].cls = 0;
-        } else if (in) {  // 0 < rel < m: floor lands in [0, m - 1]
-          const int ix = min((int)rx, mx - 1), iy = min((int)ry, my - 1), iz = min((int)rz, mz - 1);
-          t[j].wx = rx - (float)ix;
-          t[j].wy = ry - (float)iy;
-          t[j].wz = rz - (float)iz;
-          t[j].idx = (ix * g.ny + iy) * g.nz + iz;
-          t[j].cls = 1;
-        }
-      }
-    }
-    // per taxel, two bits: 0 no contact, 1 contact, 2 exact chain
-    unsigned kinds = 0;
-    int n_special = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 lo = __ldg(g.quads + t[j].idx), hi = __ldg(g.quads + t[j].idx + nyz);
-      // x lerps of the (z, z+1) x (y, y+1) corner pairs, then y, then z
-      const float e00 = fmaf(t[j].wx, hi.x - lo.x, lo.x), e01 = fmaf(t[j].wx, hi.y - lo.y, lo.y);
-      const float e10 = fmaf(t[j].wx, hi.z - lo.z, lo.z), e11 = fmaf(t[j].wx, hi.w - lo.w, lo.w);
-      const float f0 = fmaf(t[j].wy, e10 - e00, e00), f1 = fmaf(t[j].wy, e11 - e01, e01);
-      const float d32 = fmaf(t[j].wz, f1 - f0, f0);
-      const bool clear = fabsf(d32) * (1.0f - 16.0f * kU32) > 2.0f * t[j].tau;
-      const unsigned kind = t[j].cls == 0 ? 0u : (t[j].cls == 1 && clear ? (d32 < 0.0f ? 1u : 0u) : 2u);
-      kinds |= kind << (2 * j);
-      n_special += kind != 0;
-    }
     // zeros for the block's taxels, coalesced 16-B stores; contact taxels are
     // overwritten by this warp's drain (ordered by __syncwarp)
     if (full) {
@@ -556,7 +571,7 @@ __global__ void __launch_bounds__(MAXT, MINB) force_field_quad_kernel(const FFAr
       if (obb) store_zero16(obb + 3 * blk, cnt * 3 * 4 / 16, lane);
       if (ctb && lane < cnt / 4) reinterpret_cast<uchar4*>(ctb + blk)[lane] = make_uchar4(0, 0, 0, 0);
     }
-    if (__any_sync(0xffffffffu, n_special != 0)) {
+    if (__any_sync(0xffffffffu, kinds != 0)) {
       // append to the warp queue in taxel order (neighbouring taxels share
       // cells, so a drained warp's corner loads coalesce)
       const unsigned lt = (1u << lane) - 1u;
@@ -789,7 +804,7 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
       return rc;
     }
   }
-  auto launch = [&](auto out_tag) {
+  auto launch = [&](auto out_tag) -> int {
     using O = decltype(out_tag);
     const FFArgs<O> A{make_grid(sdf), taxels, n_taxels, object_state, object_stride, sensor_state, sensor_stride,
                       n_sensors, frames, P, (O*)f_n, (O*)f_t, wrench, kin, contact, obs, nullptr, taxf};
@@ -816,10 +831,10 @@ int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
     } else {
       force_field_kernel<O, 4><<<(unsigned)frames, threads, 0, s>>>(A);
     }
+    return 0;
   };
-  if (out_fp64) launch(double{});
-  else launch(float{});
-  const int launched = check_launch("force_field_kernel");
+  const int lrc = out_fp64 ? launch(double{}) : launch(float{});
+  const int launched = lrc ? lrc : check_launch("force_field_kernel");
   if (taxf) cudaFreeAsync(taxf, s);
   return launched;
 }

@@ -211,8 +211,10 @@ TACSL_API int tacsl_frame_digest(const void* data, int64_t n_frames, int64_t fra
  * z fastest (sdf.py:29-41).  Uploaded as a float64 {d, gx, gy, gz} cell grid
  * (32 B/cell, L2-resident) on `device`, so grids built in float64 by the
  * reference's build_sdf and float32 TSDF caches (sdf.py:343-344) are both
- * sampled exactly as the reference samples them.  dims >= 2 on every axis,
- * spacing > 0, else INVALID_ARGUMENT. */
+ * sampled exactly as the reference samples them, plus (when every value is
+ * finite and within float range) a float32 corner-quad grid (16 B/cell) and
+ * per-axis Lipschitz bounds for the force field's certified float32 contact
+ * test.  dims >= 2 on every axis, spacing > 0, else INVALID_ARGUMENT. */
 TACSL_API int tacsl_sdf_create(int device, const double* values, const double* gradients,
                      const int32_t dims[3], const double origin[3],
                      double spacing, tacsl_sdf_t* out);
@@ -278,6 +280,11 @@ TACSL_API int tacsl_penalty_forces(const double* d, const double* d_dot, const d
  *   obs           nullable (E, S, R, C, 3) float32 policy observation
  *                 [f_n.z, f_t.x, f_t.y] (envs/peg_tasks.py:474-476)
  * f_n / f_t may be NULL when only the wrench / observation is wanted.
+ * Contact masks are bit-exact to the reference's float64 chain whatever the
+ * path: on pads above 1024 taxels (rows*cols % 4 == 0) the call launches a
+ * float32 copy of the taxels into a stream-ordered allocation from the
+ * device's default memory pool (freed on `stream` after the kernel) and the
+ * certified float32 mask kernel; otherwise (and with kin) float64 kernels.
  */
 TACSL_API int tacsl_force_field(tacsl_sdf_t sdf, const double* taxels, int rows, int cols,
                       const double* object_state, int64_t object_stride,

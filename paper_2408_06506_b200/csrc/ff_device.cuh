@@ -404,7 +404,7 @@ struct FrameC {
   // per-frame constants of its certified error bounds
   float A32[9], b32[3];
   float amax, bmax;  // max |A_ik|, max |b_i| (rounded up)
-  float kt, k0;      // distance bound tau(p) = kt * (amax |p|_1 + bmax) + k0
+  float kt, k0;      // decision bound 2 tau / (1 - 16u) = kt * (amax |p|_1 + bmax) + k0
   // contact path in the sensor frame (unit quaternions): n_s = Mso n,
   // x_dot_s = kv + om x p  (Mso = Ms^T Mo, kv = Ms^T (s_v - o_v) - w_o,s x c_s,
   // om = Ms^T (s_w - o_w), c_s = Ms^T (s_pos - o_pos))
@@ -451,8 +451,11 @@ __device__ __forceinline__ void frame_setup_quad(const FFArgs<OutT>& A, FrameC& 
     C.amax = bad ? inf : __double2float_ru(am);
     C.bmax = bad ? inf : __double2float_ru(bm);
     constexpr float u = 5.9604645e-8f;  // 2^-24
-    C.kt = __fmul_ru(8.0f * u, g.lsum);
-    C.k0 = __fmul_ru(g.lsum, 1e-7f + 8.0f * u);
+    // tau scaled by 2 / (1 - 16u) (>= 2.0000019; the quad kernel's test is
+    // |d32| > tau, see force_field.cu)
+    constexpr float s2 = 2.0000024f;
+    C.kt = __fmul_ru(__fmul_ru(8.0f * u, g.lsum), s2);
+    C.k0 = __fmul_ru(__fmul_ru(g.lsum, 1e-7f + 8.0f * u), s2);
   }
   if (lane == 16) {
 #pragma unroll

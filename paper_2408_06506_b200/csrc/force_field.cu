@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(MAXT, MINB) force_field_fast_kernel(const FFAr
 //    lerps add at most u (4 M + lsum) with M (the cell's largest |corner|)
 //    <= |d| + lsum, so |d32 - d_ref| <= tau + 5u|d32| (+ O(u^2)), with
 //    tau = 8u lsum sb + lsum (1e-7 + 8u).  d < 0 is taken from d32 when
-//    |d32| (1 - 16u) > 2 tau; a factor-2 margin covers the rounding of the
+//    |d32| (1 - 16u) > 2 tau (the frame constants carry 2 / (1 - 16u), so
+//    the test is one compare); a factor-2 margin covers the rounding of the
 //    bound itself.
 //
 // Contact taxels then recompute the cell and d in float64 from the fast
@@ -457,9 +458,9 @@ __device__ __forceinline__ unsigned classify_block(const FFArgs<OutT>& A, const 
     int ix, iy, iz;
     {
     const bool ok = live & (sb < 1e6f);  // mrel < 1
-    in = ok & (rx >= 1.0f) & (rx < hx) & (ry >= 1.0f) & (ry < hy) & (rz >= 1.0f) & (rz < hz);
-    out = !live | (ok & ((rx < -1.0f) | (rx >= ox) | (ry < -1.0f) | (ry >= oy) | (rz < -1.0f) |
-                                    (rz >= oz)));
+    const float lo = fminf(fminf(rx, ry), rz);  // (NaN on an axis fails that axis's own tests below)
+    in = ok & (lo >= 1.0f) & (rx < hx) & (ry < hy) & (rz < hz);
+    out = !live | (ok & ((lo < -1.0f) | (rx >= ox) | (ry >= oy) | (rz >= oz)));
     // floor by round-down onto 1.5 * 2^23 (exact for rel in [1, 2^22]; only used when inside)
     const float tx = __fadd_rd(rx, kFloorMagic), ty = __fadd_rd(ry, kFloorMagic), tz = __fadd_rd(rz, kFloorMagic);
     ix = __float_as_int(tx) - 0x4B400000, iy = __float_as_int(ty) - 0x4B400000,
@@ -508,7 +509,7 @@ __device__ __forceinline__ unsigned classify_block(const FFArgs<OutT>& A, const 
     const float e10 = fmaf(t[j].wx, hi.z - lo.z, lo.z), e11 = fmaf(t[j].wx, hi.w - lo.w, lo.w);
     const float f0 = fmaf(t[j].wy, e10 - e00, e00), f1 = fmaf(t[j].wy, e11 - e01, e01);
     const float d32 = fmaf(t[j].wz, f1 - f0, f0);
-    const bool clear = fabsf(d32) * (1.0f - 16.0f * kU32) > 2.0f * t[j].tau;
+    const bool clear = fabsf(d32) > t[j].tau;  // tau here is 2 tau / (1 - 16u) (frame_setup_quad)
     const unsigned kind = t[j].cls == 0 ? 0u : (t[j].cls == 1 && clear ? (d32 < 0.0f ? 1u : 0u) : 2u);
     kinds |= kind << (2 * j);
     idx_out[j] = t[j].idx;

@@ -532,3 +532,44 @@ def test_quad_kernel_under_graph_capture(monkeypatch):
         for a, b in zip(got, (f_n, f_t, w)):
             assert torch.equal(a, b)
         assert (got[0].abs().sum() > 0).item()
+
+
+@pytest.mark.parametrize("field", ["noise", "steep", "fp64_values"])
+def test_quad_kernel_certified_mask_on_adversarial_grids(monkeypatch, field):
+    """The certified fp32 decisions on grids that are not smooth SDFs: a
+    random field with sign changes in many cells, a steep field (large
+    Lipschitz bounds), and float64 values that float32 cannot represent --
+    with random poses that put pads across the grid faces.  Masks must equal
+    the reference chain's; forces the all-exact kernel's."""
+    rng = np.random.default_rng({"noise": 1, "steep": 2, "fp64_values": 3}[field])
+    dims = (24, 20, 16)
+    h = 0.002
+    origin = np.array([-0.024, -0.02, -0.016])
+    if field == "noise":
+        v = rng.normal(0, 0.004, dims)
+    elif field == "steep":
+        v = np.tanh(rng.normal(0, 3.0, dims)) * 0.05
+    else:
+        x, y, z = np.meshgrid(*(origin[a] + h * np.arange(dims[a]) for a in range(3)), indexing="ij")
+        v = np.sqrt(x * x + y * y + z * z) - 0.011 + rng.normal(0, 1e-9, dims)  # not float32-representable
+    g = np.stack(np.gradient(v, h), axis=-1)
+    g /= np.maximum(np.linalg.norm(g, axis=-1, keepdims=True), 1e-12)
+    sdf = geometry.SdfGrid(origin=origin, spacing=h, dims=dims, values=v, gradients=g)
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 16, 20)  # 320 taxels
+    E = 96
+    obj = np.zeros((E, 13))
+    q = rng.normal(size=(E, 4))
+    obj[:, 3:7] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    obj[:, 0:3] = rng.uniform(-0.02, 0.02, (E, 3))
+    obj[:, 7:13] = rng.normal(0, 0.01, (E, 6))
+    sen = np.zeros((E, 1, 13))
+    sen[:, 0, 3] = 1.0
+    sen[:, 0, 7:13] = rng.normal(0, 0.01, (E, 6))
+    dev = torch.device("cuda")
+    tax = tactile.device_taxels(pts, dev)
+    quad = _ff_vs_exact(monkeypatch, sdf, tax, 16, 20, obj, sen)
+    assert 0 < quad[3].mean() < 1
+    rn, rt, rk = O.compute_force_field(pts.points, origin, h, dims, v, g, obj[:, 0:3], obj[:, 3:7], obj[:, 7:10],
+                                       obj[:, 10:13], sen[:, 0, 0:3], sen[:, 0, 3:7], sen[:, 0, 7:10],
+                                       sen[:, 0, 10:13])
+    assert np.array_equal(quad[3].reshape(E, 16, 20).astype(bool), rk["d"] < 0)

@@ -573,3 +573,33 @@ def test_quad_kernel_certified_mask_on_adversarial_grids(monkeypatch, field):
                                        obj[:, 10:13], sen[:, 0, 0:3], sen[:, 0, 3:7], sen[:, 0, 7:10],
                                        sen[:, 0, 10:13])
     assert np.array_equal(quad[3].reshape(E, 16, 20).astype(bool), rk["d"] < 0)
+
+
+def test_quad_kernel_fuzz_vs_exact_kernel(monkeypatch):
+    """2.6 M taxels: random poses over a sphere SDF and a noise field,
+    quad kernel vs the all-exact kernel -- identical masks, forces within
+    1e-9."""
+    rng = np.random.default_rng(7)
+    dims = (40, 36, 32)
+    h = 0.001
+    origin = -0.5 * h * (np.array(dims) - 1)
+    x, y, z = np.meshgrid(*(origin[a] + h * np.arange(dims[a]) for a in range(3)), indexing="ij")
+    fields = [np.sqrt(x * x + y * y + z * z) - 0.012, rng.normal(0, 0.002, dims)]
+    pts = sample_tactile_points(TactileSensorSpec(image_size=(320, 240)), 16, 20)
+    dev = torch.device("cuda")
+    tax = tactile.device_taxels(pts, dev)
+    E = 4096
+    for v in fields:
+        g = np.stack(np.gradient(v, h), axis=-1)
+        g /= np.maximum(np.linalg.norm(g, axis=-1, keepdims=True), 1e-12)
+        sdf = geometry.SdfGrid(origin=origin, spacing=h, dims=dims, values=v, gradients=g)
+        obj = np.zeros((E, 13))
+        q = rng.normal(size=(E, 4))
+        obj[:, 3:7] = q / np.linalg.norm(q, axis=1, keepdims=True)
+        obj[:, 0:3] = rng.uniform(-0.025, 0.025, (E, 3))
+        obj[:, 7:13] = rng.normal(0, 0.01, (E, 6))
+        sen = np.zeros((E, 1, 13))
+        sen[:, 0, 3] = 1.0
+        sen[:, 0, 7:13] = rng.normal(0, 0.01, (E, 6))
+        quad = _ff_vs_exact(monkeypatch, sdf, tax, 16, 20, obj, sen)
+        assert 0.01 < quad[3].mean() < 0.99

@@ -335,10 +335,10 @@ constexpr float kU32 = 5.9604645e-8f;  // 2^-24
 constexpr float kFloorMagic = 12582912.0f;  // 1.5 * 2^23
 
 struct QuadTaxel {
-  float wx, wy, wz;
-  int idx;
-  int cls;  // 0: outside the grid, 1: inside, 2: undecided (exact chain)
-  float tau;
+  float wx, wy, wz;  // fp32 cell weights
+  int idx;           // fp32 cell (when inside)
+  int cls;           // 0: outside the grid, 1: inside, 2: undecided (exact chain)
+  float tau;         // the decision bound 2 tau / (1 - 16u): d32 decides when |d32| > tau
 };
 
 // exact cell-validity test of one axis against the certified margin
